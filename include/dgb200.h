@@ -1,0 +1,138 @@
+/*
+ * dgb200.h -- C ABI of the B200 sparsity-aware distributed SpMM library.
+ *
+ * The reference (`distgcn` 0.1.0, /root/reference/pkg) is pure Python/NumPy
+ * with no FFI; these entry points are what its Python hot path would bind
+ * (via ctypes) to move onto the GPU.  Each one names the reference
+ * function(s) it replaces.  Plain pointers and sizes only; device pointers
+ * are marked (device).  Every function returns DG_OK (0) or a negative
+ * error code; dg_last_error() holds the message (thread-local).
+ *
+ * Streams are passed as `void*` (a cudaStream_t).  All calls are
+ * asynchronous on that stream unless stated otherwise.  Memory passed in
+ * (H, Z, halo buffers) is owned by the caller; plan objects own the
+ * device copies of the sparse operand and the exchange lists and free them
+ * in the matching *_destroy.
+ */
+#ifndef DGB200_H
+#define DGB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DG_OK 0
+#define DG_ERR_CUDA -1
+#define DG_ERR_ARG -2
+#define DG_ERR_TIMEOUT -3
+#define DG_MAX_LOCAL 64   /* ranks one process may host (virtual ranks per GPU) */
+#define DG_MAX_GROUP 64   /* members of one reduction group */
+
+const char* dg_last_error(void);
+int dg_version(void);
+/* number of kernels this library launched since load (bench's gpu_launches) */
+int64_t dg_launch_count(void);
+int dg_device_sync(void);
+
+/* ---- device memory / peers (the reference's in-process mailbox,
+ *      runtime.py:237-248, becomes symmetric device buffers) ----------- */
+int dg_malloc(void** ptr, int64_t bytes);          /* zero-filled cudaMalloc */
+int dg_free(void* ptr);
+int dg_memset0(void* ptr, int64_t bytes, void* stream);
+int dg_enable_peer(int peer_device);               /* from the current device */
+int dg_ipc_get_handle(void* dev_ptr, uint8_t handle_out[64]);
+int dg_ipc_open_handle(const uint8_t handle[64], void** dev_ptr_out);
+int dg_ipc_close(void* dev_ptr);
+
+/* ---- local SpMM: replaces sparse.local_spmm (sparse.py:208-223) and the
+ *      per-block loops of spmm._kernel_1d_* / _kernel_15d (spmm.py:172-227).
+ *
+ * One plan covers the `n_ranks` ranks hosted by this process.  Rank r's
+ * operand is its block row as CSR over an EXTENDED column space:
+ * ext < n_local[r] reads row ext of the rank's own H block; ext >= n_local[r]
+ * reads row (ext - n_local[r]) of its halo buffer (rows received from peers).
+ * Entries stay in the reference's storage order (ascending global column),
+ * which fixes the summation order: the aware and oblivious forms of a
+ * variant -- and 1.5D with c = 1 vs 1D -- are bitwise identical.
+ * Host arrays are copied; long rows are split into fixed chunks of at most
+ * `max_chunk` nonzeros and reduced in a fixed order (deterministic).     */
+typedef struct dg_spmm_plan dg_spmm_plan;
+int dg_spmm_plan_create(dg_spmm_plan** plan, int n_ranks,
+                        const int64_t* n_rows, const int64_t* n_local, const int64_t* nnz,
+                        const int64_t* const* row_ptr, const int32_t* const* col_ext,
+                        const float* const* val, int32_t max_chunk);
+int dg_spmm_plan_destroy(dg_spmm_plan* plan);
+/* info[0]=items, [1]=split rows, [2]=chunks, [3]=total nnz, [4]=device bytes */
+int dg_spmm_plan_info(const dg_spmm_plan* plan, int64_t info[8]);
+/* z[r] (n_rows[r] x ld_z, device) = A_r @ [h_local[r]; h_halo[r]] (ld_h).
+ * f <= ld_h, ld_h % 4 == 0, ld_z % 4 == 0.  acc: 0 = fp32 accumulate,
+ * 1 = fp64 accumulate.  slab_floats: feature-slab width (0 = auto: sized
+ * so one slab of the gathered rows stays L2-resident).                   */
+int dg_spmm_run(dg_spmm_plan* plan, const float* const* h_local, const float* const* h_halo,
+                float* const* z, int32_t f, int64_t ld_h, int64_t ld_z, int32_t acc,
+                int32_t slab_floats, void* stream);
+
+/* ---- halo exchange: replaces the pack `h_block[NnzCols(dst, me)]`
+ *      (spmm.py:185, 212), Comm.all_to_allv / isend / broadcast
+ *      (runtime.py:311-435) and the receiver-side `_scatter`
+ *      (spmm.py:166-169).  One fused gather + (peer) store kernel: every
+ *      segment copies rows idx[k] (or src_row0 + k when idx is NULL) of the
+ *      source rank's H into `count` consecutive rows of a destination halo
+ *      buffer, which may live on a peer GPU (P2P / CUDA-IPC mapped).       */
+typedef struct dg_xchg_plan dg_xchg_plan;
+int dg_xchg_plan_create(dg_xchg_plan** plan, int n_segs, const int32_t* src_local,
+                        const int64_t* count, const int32_t* const* idx /* host or NULL */,
+                        const int64_t* src_row0, const int32_t* dst_buf,
+                        const int64_t* dst_row0);
+int dg_xchg_plan_destroy(dg_xchg_plan* plan);
+/* dst_bufs[b] = base of halo buffer b (device; local or peer-mapped);
+ * fence_sys != 0 ends the kernel with a system-scope fence (cross-process). */
+int dg_xchg_run(dg_xchg_plan* plan, const float* const* h_src, int n_src,
+                float* const* dst_bufs, int n_dst, int32_t f, int64_t ld, int32_t fence_sys,
+                void* stream);
+
+/* ---- group all-reduce: replaces Comm.all_reduce_sum (runtime.py:437-466).
+ * For elements [lo, hi): s = src[0] + src[1] + ... (ascending member order,
+ * the reference's order), stored to every dst[m].  Each element is reduced
+ * exactly once, so all members receive bit-identical values.  Pointers may
+ * be peer-mapped; each member reduces its own slice.                      */
+int dg_group_reduce(int g, const float* const* src, float* const* dst, int64_t lo,
+                    int64_t hi, int32_t fence_sys, void* stream);
+
+/* ---- cross-process barrier over peer-mapped flag words (device-side;
+ *      one process per GPU).  flags[q] points at process q's flag array;
+ *      each process writes `epoch` to slot `me` of every peer and waits for
+ *      all slots of its own array to reach `epoch`.  Bounded by timeout_ns;
+ *      on timeout sets *err_dev = 1 instead of hanging the GPU.          */
+int dg_barrier(uint64_t* const* flags, int n_procs, int me, uint64_t epoch,
+               int64_t timeout_ns, int32_t* err_dev, void* stream);
+
+/* ---- GCN loss: replaces gcn._xent_parts (gcn.py:98-120).  Masked
+ *      softmax cross-entropy; grad = (softmax - onehot) / denom on masked
+ *      rows, 0 elsewhere; stats_out[0] += loss sum, stats_out[1] += correct
+ *      (first-index argmax, like np.argmax).  Deterministic (fixed-order
+ *      block reduction).  scratch: >= 2 * ceil(n / 8) + 2 doubles.        */
+int dg_xent(const float* logits, int64_t n, int32_t C, int64_t ld, const int64_t* labels,
+            const uint8_t* mask, double denom, float* grad, int64_t ld_grad,
+            double* scratch, uint32_t* counter, double* stats_out, void* stream);
+
+/* ---- elementwise pieces of the GCN step (gcn.py:76-82, 276, 282-283) ---- */
+int dg_relu(const float* z, float* h, int64_t rows, int32_t f, int64_t ld, void* stream);
+/* g[i, :f] *= (zprev[i, :f] > 0) */
+int dg_relu_grad_mul(float* g, int64_t ld_g, const float* zprev, int64_t ld_z,
+                     int64_t rows, int32_t f, void* stream);
+/* w -= lr * y  (n contiguous floats) */
+int dg_sgd(float* w, const float* y, int64_t n, float lr, void* stream);
+
+/* ---- host preprocessing: stable O(nnz + n) transpose, bit-identical to
+ *      sparse.transpose_csr (sparse.py:237-247).  Host pointers.          */
+int dg_host_transpose(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                      const int64_t* col, const double* val, int64_t* out_row_ptr,
+                      int64_t* out_col, double* out_val);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DGB200_H */

@@ -1,0 +1,357 @@
+"""Full-batch GCN training on the GPU -- the drop-in for `distgcn.gcn`.
+
+Same API (gcn.py:27-37): `TrainConfig`, `TrainResult`, `SerialGcn`,
+`init_weights`, `relu`, `relu_grad`, `softmax_xent`, `serial_train`,
+`train`.  The epoch loop is the reference's (gcn.py:258-286), step for
+step: per weight layer a forward multiply `spmm_kernel(fwd)` then `T W`
+and ReLU; masked softmax cross-entropy; per layer (reversed) a backward
+multiply `spmm_kernel(bwd)`, the weight gradient `H^T M` all-reduced over
+the column group, `G = (M W^T) * 1[Z > 0]` with W before its update, and
+SGD.  Every rank's data stays on the GPU for the whole run; loss and
+accuracy are accumulated on the device and read back once at the end.
+
+Numerics: fp32 storage, SpMM accumulated in fp64, GEMMs on cuBLAS fp32
+with TF32 off.  Widths are padded to multiples of 4 (zero padding, also in
+the weights) so every activation is a 16-byte-aligned row-major tensor.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .engine import _no_tf32, pad4, to_device
+from .partition import Partition, apply_partition, block_partition
+from .plan import build_dist_matrices, validate_variant_grid
+from .runtime import ProcessGrid, run_program
+from .sparse import CsrMatrix, csr_equal, local_spmm, transpose_csr
+from .spmm import exchange_index_lists, spmm_phase
+
+__all__ = ["SerialGcn", "TrainConfig", "TrainResult", "init_weights", "relu", "relu_grad",
+           "serial_train", "softmax_xent", "train"]
+
+
+@dataclass
+class TrainConfig:
+    """gcn.py:40-73.  `layers` counts representation levels: layers=3 trains
+    two weight matrices."""
+
+    layers: int = 3
+    hidden: int = 16
+    lr: float = 0.01
+    epochs: int = 100
+    activation: str = "relu"
+    seed: int = 0
+    variant: str = "1d-sparse"
+    f_in: int = None
+    f_out: int = None
+
+    def __post_init__(self):
+        if self.layers < 2:
+            raise ValueError("need at least 2 layers (one weight matrix)")
+        if self.hidden < 1:
+            raise ValueError("hidden width must be at least 1")
+        if self.lr < 0:
+            raise ValueError("learning rate must be non-negative")
+        if self.epochs < 0:
+            raise ValueError("epochs must be non-negative")
+        if self.activation != "relu":
+            raise ValueError(f"unsupported activation {self.activation!r}")
+
+    def layer_dims(self, f_in, f_out):
+        return [f_in] + [self.hidden] * (self.layers - 2) + [f_out]
+
+
+def _dev():
+    L.lib()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def relu(z):
+    """max(z, 0) on the GPU (gcn.py:76-77)."""
+    t = z if isinstance(z, torch.Tensor) else torch.from_numpy(np.asarray(z, dtype=np.float64))
+    out = torch.clamp_min(t.to(_dev()), 0.0)
+    return out if isinstance(z, torch.Tensor) else out.cpu().numpy()
+
+
+def relu_grad(z):
+    """1[z > 0] (gcn.py:80-82), 0 at exactly 0."""
+    t = z if isinstance(z, torch.Tensor) else torch.from_numpy(np.asarray(z, dtype=np.float64))
+    out = (t.to(_dev()) > 0).to(t.dtype)
+    return out if isinstance(z, torch.Tensor) else out.cpu().numpy()
+
+
+def init_weights(cfg: TrainConfig, f_in, f_out):
+    """Seeded symmetric-uniform init (gcn.py:85-95), identical draws."""
+    rng = np.random.default_rng(cfg.seed)
+    dims = cfg.layer_dims(f_in, f_out)
+    out = []
+    for fi, fo in zip(dims[:-1], dims[1:]):
+        lim = np.sqrt(6.0 / (fi + fo))
+        out.append(rng.uniform(-lim, lim, size=(fi, fo)))
+    return out
+
+
+class _Xent:
+    """Device masked softmax cross-entropy (dg_xent) with its scratch."""
+
+    def __init__(self, n, device):
+        blocks = (max(n, 1) + 7) // 8
+        self.scratch = torch.zeros(2 * blocks + 2, dtype=torch.float64, device=device)
+        self.counter = torch.zeros(1, dtype=torch.int32, device=device)
+
+    def __call__(self, logits, C, labels, mask_u8, denom, grad, stats):
+        n = logits.shape[0]
+        if n == 0:
+            return
+        L.check(L.lib().dg_xent(logits.data_ptr(), n, C, logits.stride(0), labels.data_ptr(),
+                                mask_u8.data_ptr(), float(denom), grad.data_ptr(),
+                                grad.stride(0), self.scratch.data_ptr(),
+                                self.counter.data_ptr(), stats.data_ptr(), L.stream_ptr()))
+
+
+def softmax_xent(logits, labels, mask):
+    """Mean masked cross-entropy and its gradient (gcn.py:123-132)."""
+    logits_np = np.asarray(logits, dtype=np.float64)
+    labels = np.asarray(labels)
+    mask = np.asarray(mask, dtype=bool)
+    count = int(mask.sum())
+    if count == 0:
+        raise ValueError("softmax_xent needs at least one masked row")
+    C = logits_np.shape[1]
+    sel = labels[mask]
+    if sel.min() < 0 or sel.max() >= C:
+        raise ValueError(f"labels must lie in [0, {C}) on masked rows")
+    dev = _dev()
+    ld = pad4(C)
+    x = to_device(logits_np, ld)
+    grad = torch.zeros_like(x)
+    stats = torch.zeros(2, dtype=torch.float64, device=dev)
+    _Xent(x.shape[0], dev)(x, C, torch.from_numpy(labels.astype(np.int64)).to(dev),
+                           torch.from_numpy(mask.astype(np.uint8)).to(dev), count, grad, stats)
+    st = stats.cpu().numpy()
+    return float(st[0] / count), grad[:, :C].double().cpu().numpy()
+
+
+class SerialGcn:
+    """Forward/backward on the undistributed matrix (gcn.py:135-172), on the
+    GPU; NumPy in / NumPy out like the reference."""
+
+    def __init__(self, a_hat: CsrMatrix, weights):
+        self.a = a_hat
+        at = transpose_csr(a_hat)
+        self.at = a_hat if csr_equal(at, a_hat) else at
+        self.weights = weights
+        self._cache = None
+
+    def forward(self, h0):
+        dev = _dev()
+        hs = [torch.as_tensor(np.asarray(h0, dtype=np.float64), device=dev).float()]
+        zs = []
+        last = len(self.weights) - 1
+        with _no_tf32():
+            for l, w in enumerate(self.weights):
+                t = local_spmm(self.at, hs[-1])
+                z = t @ torch.as_tensor(np.asarray(w), device=dev).float()
+                zs.append(z)
+                hs.append(torch.clamp_min(z, 0.0) if l < last else z)
+        self._cache = (hs, zs)
+        return hs[-1].double().cpu().numpy()
+
+    def backward(self, g_out):
+        if self._cache is None:
+            raise RuntimeError("backward called before forward")
+        hs, zs = self._cache
+        dev = _dev()
+        g = torch.as_tensor(np.asarray(g_out, dtype=np.float64), device=dev).float()
+        ys = [None] * len(self.weights)
+        with _no_tf32():
+            for l in range(len(self.weights) - 1, -1, -1):
+                m = local_spmm(self.a, g)
+                ys[l] = (hs[l].T @ m).double().cpu().numpy()
+                if l > 0:
+                    w = torch.as_tensor(np.asarray(self.weights[l]), device=dev).float()
+                    g = (m @ w.T) * (zs[l - 1] > 0)
+        return ys
+
+
+@dataclass
+class TrainResult:
+    """gcn.py:175-197."""
+
+    history: list
+    weights: list
+    ledger: object = None
+    partition: Partition = None
+    weights_per_rank: list = field(default_factory=list)
+
+    @property
+    def losses(self):
+        return np.array([row["loss"] for row in self.history])
+
+    @property
+    def final_accuracy(self):
+        return self.history[-1]["train_acc"] if self.history else None
+
+
+def _check_train_inputs(features, labels, train_mask):
+    n_f = features.shape[0]
+    labels = np.asarray(labels, dtype=np.int64)
+    mask = np.asarray(train_mask, dtype=bool)
+    if not (n_f == labels.shape[0] == mask.shape[0]):
+        raise ValueError("features, labels and train_mask must agree on the vertex count")
+    if int(mask.sum()) == 0:
+        raise ValueError("train_mask must select at least one vertex")
+    return labels, mask
+
+
+class GcnRun:
+    """Device state of one training run (shared by every hosted rank).
+
+    Split from `train` so the benchmark can time epochs of a prepared run
+    (setup -- partition, plans, uploads -- happens once, as in the
+    reference where it precedes the epoch loop)."""
+
+    def __init__(self, a_hat: CsrMatrix, features, labels, train_mask, cfg: TrainConfig, p=1,
+                 c=1, partition=None):
+        validate_variant_grid(cfg.variant, p, c)
+        labels, mask = _check_train_inputs(features, labels, train_mask)
+        if a_hat.n_rows != features.shape[0]:
+            raise ValueError("feature rows must match the matrix")
+        f_out = cfg.f_out if cfg.f_out is not None else int(labels.max()) + 1
+        sel = labels[mask]
+        if sel.min() < 0 or sel.max() >= f_out:
+            raise ValueError(f"labels must lie in [0, {f_out}) on masked rows")
+        self.cfg = cfg
+        self.grid = grid = ProcessGrid(p, c)
+        part = partition if partition is not None else block_partition(a_hat.n_rows,
+                                                                         grid.n_rows)
+        if part.k != grid.n_rows:
+            raise ValueError(f"partition has {part.k} parts but the grid needs {grid.n_rows}")
+        self.part = part
+        dev = _dev()
+        self.device = dev
+        is_t = isinstance(features, torch.Tensor)
+        a2, feats2 = apply_partition(a_hat, features if is_t else np.asarray(features), part)
+        inv = part.inv_perm
+        self.dm = build_dist_matrices(a2, part.boundaries, grid)
+        self.f_in = int(features.shape[1])
+        self.f_out = f_out
+        self.denom = int(mask.sum())
+        self.dims = cfg.layer_dims(self.f_in, f_out)
+        self.lds = [pad4(d) for d in self.dims]
+        w0 = init_weights(cfg, self.f_in, f_out)
+        self.w0 = []
+        for l, w in enumerate(w0):
+            wp = torch.zeros((self.lds[l], self.lds[l + 1]), dtype=torch.float32, device=dev)
+            wp[:w.shape[0], :w.shape[1]] = torch.from_numpy(w.astype(np.float32))
+            self.w0.append(wp)
+        self.x = to_device(feats2, self.lds[0])
+        lab2 = labels if part.is_identity else labels[inv]
+        msk2 = mask if part.is_identity else mask[inv]
+        self.labels = torch.from_numpy(lab2.astype(np.int64)).to(dev)
+        self.mask = torch.from_numpy(msk2.astype(np.uint8)).to(dev)
+        self.xent = {}
+
+    def program(self, comm, epochs, stats, weights_out=None):
+        """The per-rank epoch loop (gcn.py:258-286)."""
+        cfg, dm = self.cfg, self.dm
+        i, j = comm.coords
+        r0, r1 = dm.boundaries[i]
+        h0 = self.x[r0:r1]
+        yb, mb = self.labels[r0:r1], self.mask[r0:r1]
+        ws = [w.clone() for w in self.w0] if weights_out is None else weights_out
+        xent = self.xent.setdefault(comm.rank, _Xent(r1 - r0, self.device))
+        exchange_index_lists(comm, dm.fwd, cfg.variant)
+        if dm.bwd is not dm.fwd:
+            exchange_index_lists(comm, dm.bwd, cfg.variant)
+        col_group = comm.grid.col_group(j)
+        last = len(ws) - 1
+        lib = L.lib()
+        st = L.stream_ptr()
+        dims, lds = self.dims, self.lds
+        with _no_tf32():
+            for epoch in range(epochs):
+                hs, zs = [h0], []
+                for l, w in enumerate(ws):
+                    t = spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant)
+                    z = torch.mm(t, w)
+                    zs.append(z)
+                    if l < last:
+                        h = torch.empty_like(z)
+                        L.check(lib.dg_relu(z.data_ptr(), h.data_ptr(), z.shape[0],
+                                            dims[l + 1], lds[l + 1], st))
+                        hs.append(h)
+                    else:
+                        hs.append(z)
+                logits = hs[-1]
+                g = torch.empty_like(logits)
+                xent(logits, dims[-1], yb, mb, self.denom, g, stats[epoch])
+                for l in range(last, -1, -1):
+                    m = spmm_phase(comm, dm.bwd, g, dims[l + 1], cfg.variant)
+                    y = comm.all_reduce_sum(torch.mm(hs[l].T, m), group=col_group)
+                    if l > 0:
+                        g = torch.mm(m, ws[l].T)
+                        L.check(lib.dg_relu_grad_mul(g.data_ptr(), g.stride(0),
+                                                     zs[l - 1].data_ptr(), zs[l - 1].stride(0),
+                                                     g.shape[0], dims[l], st))
+                    L.check(lib.dg_sgd(ws[l].data_ptr(), y.data_ptr(), ws[l].numel(),
+                                       float(cfg.lr), st))
+                comm.ledger_mark(("epoch", epoch))
+        return {"stats": stats, "weights": ws}
+
+    def run(self, epochs=None):
+        epochs = self.cfg.epochs if epochs is None else epochs
+        p = self.grid.p
+        stats = {r: torch.zeros((max(epochs, 1), 2), dtype=torch.float64, device=self.device)
+                 for r in range(p)}
+        return run_program(p, self.grid.c, lambda comm: self.program(comm, epochs,
+                                                                     stats[comm.rank]))
+
+    def result(self, run, epochs=None) -> TrainResult:
+        epochs = self.cfg.epochs if epochs is None else epochs
+        grid = self.grid
+        per_epoch = np.zeros((epochs, 2))
+        for i in range(grid.n_rows):
+            per_epoch += run.results[grid.rank_of(i, 0)]["stats"][:epochs].cpu().numpy()
+        history = []
+        for epoch in range(epochs):
+            row = {"epoch": epoch, "loss": float(per_epoch[epoch, 0] / self.denom),
+                   "train_acc": float(per_epoch[epoch, 1] / self.denom)}
+            snap = run.ledger.marks.get(("epoch", epoch), {})
+            for prim, vals in snap.items():
+                row[f"{prim}_bytes"] = vals["bytes_sent"]
+            history.append(row)
+        wpr = []
+        for r in range(grid.p):
+            ws = run.results[r]["weights"]
+            wpr.append([w[:a, :b].double().cpu().numpy()
+                        for w, a, b in zip(ws, self.dims[:-1], self.dims[1:])])
+        return TrainResult(history, wpr[0], run.ledger, self.part, wpr)
+
+
+def train(a_hat: CsrMatrix, features, labels, train_mask, cfg: TrainConfig, p=1, c=1,
+          partition=None) -> TrainResult:
+    """Train over the selected distributed multiply variant (gcn.py:230-302),
+    every rank on the GPU.  cfg.variant == "serial" runs the undistributed
+    path (one rank, no ledger)."""
+    if cfg.variant == "serial":
+        return serial_train(a_hat, features, labels, train_mask, cfg)
+    gr = GcnRun(a_hat, features, labels, train_mask, cfg, p, c, partition)
+    run = gr.run()
+    return gr.result(run)
+
+
+def serial_train(a_hat: CsrMatrix, features, labels, train_mask, cfg: TrainConfig) -> TrainResult:
+    """Full-batch GD on one rank (gcn.py:211-227)."""
+    from dataclasses import replace
+    c2 = replace(cfg, variant="1d-sparse")
+    gr = GcnRun(a_hat, features, labels, train_mask, c2, 1, 1, None)
+    res = gr.result(gr.run())
+    for row in res.history:
+        for k in [k for k in row if k.endswith("_bytes")]:
+            del row[k]
+    return TrainResult(res.history, res.weights)

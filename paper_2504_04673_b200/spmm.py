@@ -1,0 +1,145 @@
+"""Distributed SpMM entry points -- the drop-in for `distgcn.spmm`.
+
+Same names, arguments, return types and errors as the reference
+(spmm.py:25-37): `VARIANTS`, `DistOperand`, `DistMatrices`,
+`build_dist_matrices`, `exchange_index_lists`, `spmm_kernel`, `run_spmm`,
+`serial_reference`, `validate_variant_grid`, `SpmmRun`.
+
+`spmm_kernel(comm, op, h_block, variant)` is called from inside a rank
+program exactly like the reference's; it is a collective over the ranks of
+the process, and the last rank to arrive launches the batched device phase
+(exchange -> SpMM -> 1.5D group reduction) for all of them.  The ledger is
+charged from the plan with the reference's conventions, so volumes match
+the reference bit-exactly.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .engine import DevicePlan, pad4, to_device
+from .partition import Partition, apply_partition, block_partition
+from .plan import (VARIANTS, DistMatrices, DistOperand, build_dist_matrices, build_variant_plan,
+                   index_setup_charges, validate_variant_grid)
+from .runtime import Comm, ProcessGrid, RunResult, run_program
+from .sparse import CsrMatrix, local_spmm, transpose_csr
+
+__all__ = ["DistMatrices", "DistOperand", "VARIANTS", "build_dist_matrices",
+           "exchange_index_lists", "run_spmm", "serial_reference", "spmm_kernel",
+           "validate_variant_grid", "SpmmRun", "device_plan", "spmm_phase"]
+
+
+def exchange_index_lists(comm: Comm, op: DistOperand, variant: str):
+    """One-time NnzCols announcements (spmm.py:133-163).  The lists are
+    already known to every host (the plan is deterministic), so nothing
+    moves on the device; the reference's index traffic is charged once,
+    by whichever rank arrives last."""
+    grid = comm.grid
+    ledger = comm.ledger
+
+    def complete(arr):
+        index_setup_charges(ledger, op, grid, variant)
+        return {r: None for r in arr}
+
+    comm._collective(("idx", id(op), variant), tuple(range(comm.p)), None, complete)
+
+
+def device_plan(op: DistOperand, grid: ProcessGrid, variant: str, local_ranks=None):
+    """Device plan of `op` for `variant`, built once and cached on the operand."""
+    key = (variant, grid.p, grid.c, torch.cuda.current_device(),
+           None if local_ranks is None else tuple(local_ranks))
+    dp = op._device.get(key)
+    if dp is None:
+        dp = DevicePlan(build_variant_plan(op, grid, variant), local_ranks)
+        op._device[key] = dp
+    return dp
+
+
+def spmm_phase(comm: Comm, op: DistOperand, h_pad: torch.Tensor, f: int, variant: str):
+    """Device form of `spmm_kernel`: h_pad is a contiguous fp32 CUDA tensor
+    (n_i, pad4(f)) with zero padding; returns the padded (n_i, pad4(f))
+    product.  A collective over the ranks of this process: the last rank to
+    arrive launches exchange -> SpMM -> (1.5D) group reduction for all."""
+    grid = comm.grid
+    ledger = comm.ledger
+    ld = pad4(f)
+
+    def complete(arr):
+        dp = device_plan(op, grid, variant)
+        hs = {}
+        for r, h in arr.items():
+            hs[r] = h if (isinstance(h, torch.Tensor) and h.dtype == torch.float32
+                          and h.is_cuda and h.is_contiguous() and h.shape[1] == ld) \
+                else to_device(h[:, :f], ld)
+        out = dp.run(hs, f, ld)
+        dp.vplan.charge(ledger, f)
+        return out
+
+    return comm._collective(("spmm", id(op), variant), tuple(range(comm.p)), h_pad, complete)
+
+
+def spmm_kernel(comm: Comm, op: DistOperand, h_block, variant: str):
+    """One distributed multiply phase from inside a rank program
+    (spmm.py:230-246).  h_block: this rank's block row of H (NumPy array or
+    CUDA tensor, replicated over the row group when c > 1).  Returns the
+    block row of the product: a CUDA tensor (n_i, f) for tensor input, a
+    float64 NumPy array for NumPy input."""
+    if variant not in VARIANTS:
+        raise ValueError(f"unknown variant {variant!r}; expected one of {VARIANTS}")
+    numpy_in = not isinstance(h_block, torch.Tensor)
+    f = int(h_block.shape[1])
+    z = spmm_phase(comm, op, to_device(h_block, pad4(f)), f, variant)
+    if numpy_in:
+        return z[:, :f].double().cpu().numpy()
+    return z if z.shape[1] == f else z[:, :f]
+
+
+def serial_reference(a: CsrMatrix, h) -> np.ndarray:
+    """transpose(a) @ h on one GPU (spmm.py:249-252)."""
+    return local_spmm(transpose_csr(a), h)
+
+
+@dataclass
+class SpmmRun:
+    z: np.ndarray
+    ledger: object
+    dm: DistMatrices
+    partition: Partition
+    grid: ProcessGrid
+
+
+def run_spmm(a: CsrMatrix, h, p, c, variant, partition=None, index_setup=True) -> SpmmRun:
+    """One distributed multiply end to end (spmm.py:264-294): permute by the
+    partition (block by default), distribute on the (p/c) x c grid, run the
+    variant on the GPU, gather back in the original order."""
+    validate_variant_grid(variant, p, c)
+    if a.n_rows != a.n_cols:
+        raise ValueError("distributed multiply requires a square matrix")
+    numpy_in = not isinstance(h, torch.Tensor)
+    if numpy_in:
+        h = np.asarray(h, dtype=np.float64)
+    grid = ProcessGrid(p, c)
+    part = partition if partition is not None else block_partition(a.n_rows, grid.n_rows)
+    if part.k != grid.n_rows:
+        raise ValueError(f"partition has {part.k} parts but the grid needs {grid.n_rows}")
+    a2, h2 = apply_partition(a, h, part)
+    dm = build_dist_matrices(a2, part.boundaries, grid)
+    f = int(h2.shape[1])
+    hd = to_device(h2, pad4(f))
+
+    def program(comm):
+        i, _ = comm.coords
+        r0, r1 = dm.boundaries[i]
+        if index_setup:
+            exchange_index_lists(comm, dm.fwd, variant)
+        return spmm_phase(comm, dm.fwd, hd[r0:r1], f, variant)
+
+    run: RunResult = run_program(p, c, program)
+    z2 = torch.cat([run.results[grid.rank_of(i, 0)] for i in range(grid.n_rows)], 0)[:, :f]
+    if not part.is_identity:
+        z2 = z2[torch.from_numpy(part.perm).to(z2.device)]
+    z = z2.double().cpu().numpy() if numpy_in else z2
+    return SpmmRun(z, run.ledger, dm, part, grid)
