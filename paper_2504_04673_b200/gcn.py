@@ -292,7 +292,8 @@ class GcnRun:
                 xent(logits, dims[-1], yb, mb, self.denom, g, stats[epoch])
                 for l in range(last, -1, -1):
                     m = spmm_phase(comm, dm.bwd, g, dims[l + 1], cfg.variant)
-                    y = comm.all_reduce_sum(torch.mm(hs[l].T, m), group=col_group)
+                    y = comm.all_reduce_sum(torch.mm(hs[l].T, m), group=col_group,
+                                            elems=dims[l] * dims[l + 1])
                     if l > 0:
                         g = torch.mm(m, ws[l].T)
                         L.check(lib.dg_relu_grad_mul(g.data_ptr(), g.stride(0),

@@ -1,0 +1,68 @@
+"""Profile helper: build a benchmark graph and run the local SpMM at given
+widths / slab widths (timing sweeps and the ncu target).
+
+    python scripts/prof_spmm.py --workload reddit --f 602 16 --reps 3 [--acc 1] [--slab 0]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_2504_04673_b200 as P  # noqa: E402
+from paper_2504_04673_b200 import _lib as L  # noqa: E402
+from paper_2504_04673_b200.engine import pad4  # noqa: E402
+from paper_2504_04673_b200.spmm import device_plan  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="reddit")
+    ap.add_argument("--f", type=int, nargs="+", default=[602])
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--acc", type=int, nargs="+", default=[1])
+    ap.add_argument("--slab", type=int, nargs="+", default=[0])
+    ap.add_argument("--chunk", type=int, default=0)
+    args = ap.parse_args()
+    torch.cuda.set_device(0)
+    a = bench.make_graph(args.workload)
+    grid = P.ProcessGrid(1, 1)
+    dm = P.build_dist_matrices(a, [(0, a.n_rows)], grid)
+    if args.chunk:
+        import paper_2504_04673_b200.engine as E
+        E.MAX_CHUNK = args.chunk
+    dp = device_plan(dm.fwd, grid, "1d-sparse")
+    lib = L.lib()
+    for f in args.f:
+        ld = pad4(f)
+        h = torch.randn((a.n_rows, ld), device="cuda")
+        h[:, f:] = 0
+        z = torch.empty_like(h)
+        for acc in args.acc:
+            for slab in args.slab:
+                def go():
+                    L.check(lib.dg_spmm_run(dp._splan, L.ptr_array([h]), L.ptr_array([h]),
+                                            L.ptr_array([z]), f, ld, ld, acc, slab,
+                                            L.stream_ptr()))
+                go()
+                torch.cuda.synchronize()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(args.reps):
+                    go()
+                e1.record()
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) / args.reps
+                gather = 4.0 * f * a.nnz
+                print(f"f={f} slab={slab} acc={acc} chunk={args.chunk}: {t:.3f} ms  "
+                      f"gather {gather / t / 1e6:.0f} GB/s  nnz*f/s {a.nnz * f / t / 1e6:.3g} G",
+                      flush=True)
+
+
+if __name__ == "__main__":
+    main()
