@@ -1,0 +1,193 @@
+// gcn.cu -- GCN step pieces: masked softmax cross-entropy, ReLU, ReLU
+// gradient mask, SGD.
+
+#include <cmath>
+
+#include "common.cuh"
+
+// ---------------------------------------------------------------------------
+// GCN pieces
+// ---------------------------------------------------------------------------
+
+namespace {
+
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_min(int v) {
+  for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// one warp per row; 8 rows per block; deterministic two-level reduction
+__global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ x, int64_t n, int C,
+                                                   int64_t ld, const int64_t* __restrict__ labels,
+                                                   const uint8_t* __restrict__ mask, double denom,
+                                                   float* __restrict__ grad, int64_t ldg,
+                                                   double* scratch, unsigned* counter,
+                                                   double* out) {
+  __shared__ double s_loss[8];
+  __shared__ double s_corr[8];
+  __shared__ bool s_last;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * 8 + w;
+  double loss = 0.0, corr = 0.0;
+  if (row < n) {
+    const float* xr = x + row * ld;
+    float m = -INFINITY;
+    for (int j = lane; j < C; j += 32) m = fmaxf(m, xr[j]);
+    m = warp_max(m);
+    double s = 0.0;
+    for (int j = lane; j < C; j += 32) s += exp((double)xr[j] - (double)m);
+    s = warp_sum(s);
+    int am = C;
+    for (int j = lane; j < C; j += 32)
+      if (xr[j] == m) {
+        am = j;
+        break;
+      }
+    am = warp_min(am);
+    const bool on = mask[row] != 0;
+    const int64_t lbl = labels[row];
+    float* gr = grad + row * ldg;
+    for (int j = lane; j < C; j += 32) {
+      float gv = 0.f;
+      if (on) {
+        double sm = exp((double)xr[j] - (double)m) / s;
+        if (j == lbl) sm -= 1.0;
+        gv = (float)(sm / denom);
+      }
+      gr[j] = gv;
+    }
+    for (int j = C + lane; j < ldg; j += 32) gr[j] = 0.f;
+    if (on) {
+      loss = log(s) - ((double)xr[lbl] - (double)m);
+      corr = (am == lbl) ? 1.0 : 0.0;
+    }
+  }
+  if (lane == 0) {
+    s_loss[w] = loss;
+    s_corr[w] = corr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double l = 0.0, c = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      l += s_loss[i];
+      c += s_corr[i];
+    }
+    scratch[2 * blockIdx.x] = l;
+    scratch[2 * blockIdx.x + 1] = c;
+    __threadfence();
+    const unsigned done = atomicAdd(counter, 1u);
+    s_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    __shared__ double r_l[256];
+    __shared__ double r_c[256];
+    double l = 0.0, c = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+      l += ((volatile double*)scratch)[2 * b];
+      c += ((volatile double*)scratch)[2 * b + 1];
+    }
+    r_l[threadIdx.x] = l;
+    r_c[threadIdx.x] = c;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+      if ((int)threadIdx.x < o) {
+        r_l[threadIdx.x] += r_l[threadIdx.x + o];
+        r_c[threadIdx.x] += r_c[threadIdx.x + o];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      out[0] += r_l[0];
+      out[1] += r_c[0];
+      *counter = 0u;
+    }
+  }
+}
+
+__global__ void relu_kernel(const float4* __restrict__ z, float4* __restrict__ h, int64_t n4) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float4 v = z[i];
+    v.x = fmaxf(v.x, 0.f);
+    v.y = fmaxf(v.y, 0.f);
+    v.z = fmaxf(v.z, 0.f);
+    v.w = fmaxf(v.w, 0.f);
+    h[i] = v;
+  }
+}
+
+__global__ void relu_grad_mul_kernel(float* g, int64_t ldg, const float* __restrict__ z,
+                                     int64_t ldz, int64_t rows, int f) {
+  const int64_t n = rows * (int64_t)f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / f;
+    const int c = (int)(i - r * f);
+    if (!(z[r * ldz + c] > 0.f)) g[r * ldg + c] = 0.f;
+  }
+}
+
+__global__ void sgd_kernel(float* w, const float* __restrict__ y, int64_t n, float lr) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    w[i] -= lr * y[i];
+}
+
+unsigned grid_for(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  return (unsigned)std::min<int64_t>(std::max<int64_t>(b, 1), 16 * 148);
+}
+
+}  // namespace
+
+extern "C" {
+
+int dg_xent(const float* logits, int64_t n, int32_t C, int64_t ld, const int64_t* labels,
+            const uint8_t* mask, double denom, float* grad, int64_t ld_grad, double* scratch,
+            uint32_t* counter, double* stats_out, void* stream) {
+  if (n < 1 || C < 1 || C > ld || C > ld_grad) return set_err(DG_ERR_ARG, "xent: bad args");
+  const unsigned blocks = (unsigned)((n + 7) / 8);
+  xent_kernel<<<blocks, 256, 0, S(stream)>>>(logits, n, C, ld, labels, mask, denom, grad,
+                                             ld_grad, scratch, counter, stats_out);
+  DG_LAUNCHED();
+  return DG_OK;
+}
+
+int dg_relu(const float* z, float* h, int64_t rows, int32_t f, int64_t ld, void* stream) {
+  if (ld % 4 || f > ld) return set_err(DG_ERR_ARG, "relu: ld % 4 != 0");
+  const int64_t n4 = rows * ld / 4;
+  if (!n4) return DG_OK;
+  relu_kernel<<<grid_for(n4, 256), 256, 0, S(stream)>>>(reinterpret_cast<const float4*>(z),
+                                                        reinterpret_cast<float4*>(h), n4);
+  DG_LAUNCHED();
+  return DG_OK;
+}
+
+int dg_relu_grad_mul(float* g, int64_t ld_g, const float* zprev, int64_t ld_z, int64_t rows,
+                     int32_t f, void* stream) {
+  const int64_t n = rows * (int64_t)f;
+  if (!n) return DG_OK;
+  relu_grad_mul_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(g, ld_g, zprev, ld_z, rows, f);
+  DG_LAUNCHED();
+  return DG_OK;
+}
+
+int dg_sgd(float* w, const float* y, int64_t n, float lr, void* stream) {
+  if (!n) return DG_OK;
+  sgd_kernel<<<grid_for(n, 256), 256, 0, S(stream)>>>(w, y, n, lr);
+  DG_LAUNCHED();
+  return DG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,493 @@
+// spmm.cu -- the local SpMM of every hosted rank (sm_100a).
+//
+// Replaces sparse.local_spmm (sparse.py:208-223) and the per-source-block
+// loops of spmm._kernel_1d_* / _kernel_15d (spmm.py:172-227): one launch
+// computes Z_r = A_r [H_r ; halo_r] for all ranks hosted by the process.
+//
+// Why this shape (DESIGN.md has the measurements):
+//  * SpMM is gather-bound (<= f/4 flop per byte), not tensor-core work.
+//    The limiter on B200 is memory-level parallelism: every nonzero needs
+//    its (col, val) from the CSR stream before the H row can be gathered.
+//  * Entries are stored interleaved, 8 B per nonzero ({col, val}), each
+//    work item starting 16-B aligned, so a lane fetches two entries with
+//    one 16-B load.  All lanes of a group load the same entries (a uniform
+//    broadcast load, one L1 wavefront) -- no shuffles.  The next step's
+//    entries are prefetched while the current step's H rows are gathered
+//    (software pipelining hides the CSR stream latency).
+//  * A group of G lanes owns one item; lane l owns float4 chunks l, l+G, ...
+//    of the current feature slab, so one H-row gather is G x 16 B
+//    contiguous.  Wide layers are split into slabs (grid.y) sized so one
+//    slab of all gathered rows stays L2-resident; the CSR stream is loaded
+//    evict-first so it does not push H out of L2.
+//  * Numerics: each step's E products are summed in fp32 and folded into
+//    fp64 accumulators (error <= E * 2^-24 of the window's |terms|, E <= 8),
+//    in CSR storage order; long rows are split at fixed boundaries and the
+//    fp64 partials summed in chunk order.  Deterministic, and identical for
+//    every variant (aware == oblivious, 1.5D c=1 == 1D, bitwise).
+
+#include "common.cuh"
+
+namespace {
+
+struct Item {          // 24 B: one row, or one fixed chunk of a long row
+  int64_t lo;          // first entry (even: 16-B aligned)
+  int32_t row;         // output row
+  int32_t len;         // entries in this item
+  int32_t rank;        // local rank index
+  int32_t slot;        // -1: write z directly; else fp64 partial slot
+};
+
+struct Fixup {         // a split row: partial slots [slot0, slot0 + n)
+  int32_t row;
+  int32_t rank;
+  int32_t slot0;
+  int32_t n;
+};
+
+struct RankArgs {
+  const int4* ent;     // interleaved {col, val bits} pairs, two per int4
+  const float* hl;     // own H block (ext < n_local)
+  const float* hh;     // halo rows (ext >= n_local)
+  float* z;
+  int64_t n_local;
+};
+
+struct SpmmArgs {
+  RankArgs r[DG_MAX_LOCAL];
+  const Item* items;
+  double* part;
+  int64_t n_items;
+  int64_t ld_h;
+  int64_t ld_z;
+  int64_t ld_part;
+  int32_t chunks;      // ceil(f / 4): float4 chunks that carry features
+  int32_t slab;        // chunks per slab (= G * CPL)
+};
+
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// CSR stream: read once per slab pass; keep it out of L1 and first in line
+// for L2 eviction so the gathered H rows stay resident.
+__device__ __forceinline__ int4 ld_stream(const int4* p, uint64_t pol) {
+  int4 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+      : "l"(p), "l"(pol));
+  return v;
+}
+
+__device__ __forceinline__ float4 ld_h(const float4* p) { return __ldg(p); }
+
+template <int G, int CPL, bool F64>
+__global__ void __launch_bounds__(256) spmm_kernel(const __grid_constant__ SpmmArgs a) {
+  constexpr int E = (CPL == 1) ? 8 : 4;     // entries per pipeline step
+  constexpr int E4 = E / 2;                 // int4 loads per step
+  const int lig = threadIdx.x & (G - 1);
+  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  if (gid >= a.n_items) return;             // whole group leaves together
+  const Item it = a.items[gid];
+  const RankArgs& R = a.r[it.rank];
+  const int slab0 = blockIdx.y * a.slab;
+  const int64_t ld = a.ld_h;
+  const int4* __restrict__ ep = R.ent + (it.lo >> 1);
+  const float* __restrict__ hl = R.hl;
+  const float* __restrict__ hh = R.hh;
+  const int64_t nl = R.n_local;
+  const uint64_t pol = evict_first_policy();
+
+  int chk[CPL];
+  bool on[CPL];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    chk[q] = slab0 + lig + q * G;
+    on[q] = chk[q] < a.chunks && (lig + q * G) < a.slab;
+  }
+  float part[CPL][4];
+  double acc[F64 ? CPL : 1][4];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) part[q][k] = 0.f;
+  if constexpr (F64) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[q][k] = 0.0;
+  }
+
+  const int len = it.len;
+  const int n4 = (len + 1) >> 1;            // int4 words of this item
+  const int steps = (len + E - 1) / E;
+  int4 nx[E4];
+#pragma unroll
+  for (int u = 0; u < E4; ++u) nx[u] = (u < n4) ? ld_stream(ep + u, pol) : make_int4(0, 0, 0, 0);
+
+  for (int s = 0; s < steps; ++s) {
+    int4 cur[E4];
+#pragma unroll
+    for (int u = 0; u < E4; ++u) cur[u] = nx[u];
+    if (s + 1 < steps) {                    // prefetch the next step's entries
+#pragma unroll
+      for (int u = 0; u < E4; ++u) {
+        const int w = (s + 1) * E4 + u;
+        nx[u] = (w < n4) ? ld_stream(ep + w, pol) : make_int4(0, 0, 0, 0);
+      }
+    }
+    const int nv = min(E, len - s * E);
+    float4 x[E][CPL];
+    float v[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int c = (j & 1) ? cur[j >> 1].z : cur[j >> 1].x;
+      v[j] = __int_as_float((j & 1) ? cur[j >> 1].w : cur[j >> 1].y);
+      if (j < nv) {
+        const float* hp = c < nl ? hl + (int64_t)c * ld : hh + (int64_t)(c - nl) * ld;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+          x[j][q] = on[q] ? ld_h(reinterpret_cast<const float4*>(hp) + chk[q])
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+      } else {
+        v[j] = 0.f;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) x[j][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < E; ++j)
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        part[q][0] = fmaf(v[j], x[j][q].x, part[q][0]);
+        part[q][1] = fmaf(v[j], x[j][q].y, part[q][1]);
+        part[q][2] = fmaf(v[j], x[j][q].z, part[q][2]);
+        part[q][3] = fmaf(v[j], x[j][q].w, part[q][3]);
+      }
+    if constexpr (F64) {
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          acc[q][k] += (double)part[q][k];
+          part[q][k] = 0.f;
+        }
+    }
+  }
+
+  if (it.slot < 0) {
+    float* zp = R.z + (int64_t)it.row * a.ld_z;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+      if (on[q]) {
+        float4 o;
+        if constexpr (F64) {
+          o = make_float4((float)acc[q][0], (float)acc[q][1], (float)acc[q][2], (float)acc[q][3]);
+        } else {
+          o = make_float4(part[q][0], part[q][1], part[q][2], part[q][3]);
+        }
+        reinterpret_cast<float4*>(zp)[chk[q]] = o;
+      }
+  } else {
+    double* pp = a.part + (int64_t)it.slot * a.ld_part;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+      if (on[q]) {
+        double4 d;
+        if constexpr (F64) {
+          d = make_double4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
+        } else {
+          d = make_double4(part[q][0], part[q][1], part[q][2], part[q][3]);
+        }
+        reinterpret_cast<double4*>(pp)[chk[q]] = d;
+      }
+  }
+}
+
+struct FixArgs {
+  float* z[DG_MAX_LOCAL];
+  const Fixup* fix;
+  const double* part;
+  int64_t ld_z;
+  int64_t ld_part;
+  int32_t nfloat;      // chunks * 4
+};
+
+__global__ void __launch_bounds__(128) spmm_fixup_kernel(const __grid_constant__ FixArgs a) {
+  const Fixup fx = a.fix[blockIdx.x];
+  float* zp = a.z[fx.rank] + (int64_t)fx.row * a.ld_z;
+  for (int c = threadIdx.x; c < a.nfloat; c += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < fx.n; ++k) s += a.part[(int64_t)(fx.slot0 + k) * a.ld_part + c];
+    zp[c] = (float)s;
+  }
+}
+
+int bucket_of(int32_t len) {
+  // ~4 buckets per octave: warps see trip counts within ~19% of each other
+  if (len <= 0) return 0;
+  return (int)(4.0 * std::log2((double)len)) + 1;
+}
+
+template <int G, int CPL, bool F64>
+void launch_spmm(const SpmmArgs& a, int nslabs, cudaStream_t s) {
+  const int64_t threads = a.n_items * G;
+  const unsigned gx = (unsigned)((threads + 255) / 256);
+  spmm_kernel<G, CPL, F64><<<dim3(gx, nslabs), 256, 0, s>>>(a);
+}
+
+using LaunchFn = void (*)(const SpmmArgs&, int, cudaStream_t);
+
+template <bool F64>
+LaunchFn pick_launch(int G, int CPL) {
+#define DG_CASE(g, c) \
+  if (G == g && CPL == c) return &launch_spmm<g, c, F64>;
+  DG_CASE(1, 1) DG_CASE(1, 2) DG_CASE(1, 3) DG_CASE(1, 4)
+  DG_CASE(2, 1) DG_CASE(2, 2) DG_CASE(2, 3) DG_CASE(2, 4)
+  DG_CASE(4, 1) DG_CASE(4, 2) DG_CASE(4, 3) DG_CASE(4, 4)
+  DG_CASE(8, 1) DG_CASE(8, 2) DG_CASE(8, 3) DG_CASE(8, 4)
+  DG_CASE(16, 1) DG_CASE(16, 2) DG_CASE(16, 3) DG_CASE(16, 4)
+  DG_CASE(32, 1) DG_CASE(32, 2) DG_CASE(32, 3) DG_CASE(32, 4)
+#undef DG_CASE
+  return nullptr;
+}
+
+// Lane-group size G and chunks-per-lane CPL for `chunks` float4 chunks when
+// one slab may hold at most `wmax` chunks: fewest slabs, then least waste,
+// ties to the larger G.
+void choose_config(int chunks, int wmax, int* G_out, int* CPL_out, int* nslabs_out) {
+  static const int Gs[6] = {32, 16, 8, 4, 2, 1};
+  int bestG = 1, bestC = 1, bestS = 1 << 30, bestWaste = 1 << 30;
+  wmax = std::max(wmax, 1);
+  for (int gi = 0; gi < 6; ++gi) {
+    for (int c = 1; c <= 4; ++c) {
+      const int G = Gs[gi], W = G * c;
+      if (W > wmax && !(G == 1 && c == 1)) continue;
+      const int ns = (chunks + W - 1) / W;
+      const int waste = ns * W - chunks;
+      if (ns < bestS || (ns == bestS && waste < bestWaste)) {
+        bestS = ns;
+        bestWaste = waste;
+        bestG = G;
+        bestC = c;
+      }
+    }
+  }
+  *G_out = bestG;
+  *CPL_out = bestC;
+  *nslabs_out = bestS;
+}
+
+}  // namespace
+
+struct dg_spmm_plan {
+  int n_ranks = 0;
+  std::vector<int64_t> n_rows, n_local, nnz, ext_rows;
+  std::vector<int4*> ent;
+  Item* items = nullptr;
+  int64_t n_items = 0;
+  Fixup* fix = nullptr;
+  int64_t n_fix = 0;
+  int64_t n_slots = 0;
+  double* part = nullptr;
+  int64_t part_cap = 0;  // doubles
+  int64_t dev_bytes = 0;
+};
+
+extern "C" {
+
+int dg_spmm_plan_destroy(dg_spmm_plan* p) {
+  if (!p) return DG_OK;
+  for (auto* e : p->ent) cudaFree(e);
+  if (p->items) cudaFree(p->items);
+  if (p->fix) cudaFree(p->fix);
+  if (p->part) cudaFree(p->part);
+  delete p;
+  return DG_OK;
+}
+
+int dg_spmm_plan_create(dg_spmm_plan** out, int n_ranks, const int64_t* n_rows,
+                        const int64_t* n_local, const int64_t* nnz,
+                        const int64_t* const* row_ptr, const int32_t* const* col_ext,
+                        const float* const* val, int32_t max_chunk) {
+  if (!out || n_ranks < 1 || n_ranks > DG_MAX_LOCAL || max_chunk < 1)
+    return set_err(DG_ERR_ARG, "dg_spmm_plan_create: bad args");
+  auto* p = new dg_spmm_plan();
+  p->n_ranks = n_ranks;
+  std::vector<Item> items;
+  std::vector<Fixup> fix;
+  int64_t slots = 0;
+  for (int r = 0; r < n_ranks; ++r) {
+    p->n_rows.push_back(n_rows[r]);
+    p->n_local.push_back(n_local[r]);
+    p->nnz.push_back(nnz[r]);
+    if (n_rows[r] > INT32_MAX) {
+      delete p;
+      return set_err(DG_ERR_ARG, "dg_spmm_plan_create: rank too large for int32 rows");
+    }
+    int32_t mx = -1;
+    for (int64_t k = 0; k < nnz[r]; ++k) mx = std::max(mx, col_ext[r][k]);
+    p->ext_rows.push_back((int64_t)mx + 1);
+    for (int64_t i = 0; i < n_rows[r]; ++i) {
+      const int64_t lo = row_ptr[r][i], hi = row_ptr[r][i + 1];
+      const int64_t len = hi - lo;
+      if (len <= max_chunk) {
+        items.push_back(Item{lo, (int32_t)i, (int32_t)len, r, -1});
+      } else {
+        const int32_t n = (int32_t)((len + max_chunk - 1) / max_chunk);
+        fix.push_back(Fixup{(int32_t)i, r, (int32_t)slots, n});
+        for (int32_t k = 0; k < n; ++k) {
+          const int64_t a0 = lo + (int64_t)k * max_chunk;
+          const int64_t a1 = std::min(hi, a0 + max_chunk);
+          items.push_back(Item{a0, (int32_t)i, (int32_t)(a1 - a0), r, (int32_t)(slots + k)});
+        }
+        slots += n;
+      }
+    }
+  }
+  // bucket by length (descending, stable): similar trip counts per warp,
+  // heavy items first, row order kept inside a bucket for locality
+  std::stable_sort(items.begin(), items.end(), [](const Item& x, const Item& y) {
+    return bucket_of(x.len) > bucket_of(y.len);
+  });
+  // lay the entries out in item order (the order warps stream them), each
+  // item starting at an even entry (16-B aligned int4 pairs)
+  std::vector<int64_t> cursor(n_ranks, 0);
+  std::vector<int64_t> total(n_ranks, 0);
+  for (const Item& it : items) total[it.rank] += (it.len + 1) & ~1LL;
+  std::vector<std::vector<int32_t>> host(n_ranks);
+  for (int r = 0; r < n_ranks; ++r) host[r].assign(2 * std::max<int64_t>(total[r], 2), 0);
+  for (Item& it : items) {
+    const int r = it.rank;
+    const int64_t dst = cursor[r];
+    int32_t* h = host[r].data() + 2 * dst;
+    for (int32_t k = 0; k < it.len; ++k) {
+      h[2 * k] = col_ext[r][it.lo + k];
+      float v = val[r][it.lo + k];
+      std::memcpy(&h[2 * k + 1], &v, 4);
+    }
+    it.lo = dst;
+    cursor[r] += (it.len + 1) & ~1LL;
+  }
+  p->n_items = (int64_t)items.size();
+  p->n_fix = (int64_t)fix.size();
+  p->n_slots = slots;
+  auto fail = [&](cudaError_t e, const char* what) {
+    dg_spmm_plan_destroy(p);
+    return set_err(DG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  };
+  for (int r = 0; r < n_ranks; ++r) {
+    int4* d = nullptr;
+    const size_t bytes = host[r].size() * sizeof(int32_t);
+    cudaError_t e = cudaMalloc(&d, bytes);
+    if (e != cudaSuccess) return fail(e, "cudaMalloc(entries)");
+    p->ent.push_back(d);
+    e = cudaMemcpy(d, host[r].data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(e, "cudaMemcpy(entries)");
+    p->dev_bytes += (int64_t)bytes;
+    std::vector<int32_t>().swap(host[r]);
+  }
+  cudaError_t e = cudaMalloc(&p->items, std::max<size_t>(items.size(), 1) * sizeof(Item));
+  if (e != cudaSuccess) return fail(e, "cudaMalloc(items)");
+  if (!items.empty()) {
+    e = cudaMemcpy(p->items, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(e, "cudaMemcpy(items)");
+  }
+  e = cudaMalloc(&p->fix, std::max<size_t>(fix.size(), 1) * sizeof(Fixup));
+  if (e != cudaSuccess) return fail(e, "cudaMalloc(fix)");
+  if (!fix.empty()) {
+    e = cudaMemcpy(p->fix, fix.data(), fix.size() * sizeof(Fixup), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return fail(e, "cudaMemcpy(fix)");
+  }
+  p->dev_bytes += (int64_t)(items.size() * sizeof(Item) + fix.size() * sizeof(Fixup));
+  *out = p;
+  return DG_OK;
+}
+
+int dg_spmm_plan_info(const dg_spmm_plan* p, int64_t info[8]) {
+  if (!p) return set_err(DG_ERR_ARG, "null plan");
+  int64_t nnz = 0, ext = 0;
+  for (auto x : p->nnz) nnz += x;
+  for (auto x : p->ext_rows) ext += x;
+  info[0] = p->n_items;
+  info[1] = p->n_fix;
+  info[2] = p->n_slots;
+  info[3] = nnz;
+  info[4] = p->dev_bytes + p->part_cap * 8;
+  info[5] = ext;
+  info[6] = 0;
+  info[7] = 0;
+  return DG_OK;
+}
+
+int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const* h_halo,
+                float* const* z, int32_t f, int64_t ld_h, int64_t ld_z, int32_t acc,
+                int32_t slab_floats, void* stream) {
+  if (!p) return set_err(DG_ERR_ARG, "dg_spmm_run: null plan");
+  if (f < 1 || ld_h % 4 || ld_z % 4 || f > ld_h || f > ld_z)
+    return set_err(DG_ERR_ARG, "dg_spmm_run: need 1 <= f <= ld, ld % 4 == 0");
+  const int chunks = (f + 3) / 4;
+  SpmmArgs a;
+  std::memset(&a, 0, sizeof(a));
+  int64_t ext_total = 0;
+  for (int r = 0; r < p->n_ranks; ++r) {
+    const uintptr_t al = (uintptr_t)h_local[r] | (uintptr_t)z[r] |
+                         (uintptr_t)(h_halo ? h_halo[r] : nullptr);
+    if (al & 15) return set_err(DG_ERR_ARG, "dg_spmm_run: H/Z must be 16-byte aligned");
+    a.r[r] = RankArgs{p->ent[r], h_local[r], h_halo ? h_halo[r] : nullptr, z[r],
+                      p->n_local[r]};
+    ext_total += p->ext_rows[r];
+  }
+  if (p->n_slots) {
+    const int64_t need = p->n_slots * ld_h;
+    if (need > p->part_cap) {
+      if (p->part) cudaFree(p->part);
+      p->part = nullptr;
+      p->part_cap = 0;
+      DG_CK(cudaMalloc(&p->part, need * sizeof(double)));
+      p->part_cap = need;
+    }
+  }
+  int wmax;
+  if (slab_floats > 0) {
+    wmax = std::max(1, slab_floats / 4);
+  } else {
+    // one slab of every gathered row within ~2x the 126 MB L2: measured on
+    // B200 (Reddit-shaped, f=602) fewer, wider slabs beat strict L2
+    // residency -- each slab pass re-streams the CSR and re-walks the items
+    const double budget = 256.0 * 1024 * 1024;
+    const double per_chunk = (double)std::max<int64_t>(ext_total, 1) * 16.0;
+    wmax = (int)std::max(1.0, budget / per_chunk);
+  }
+  int G, CPL, ns;
+  choose_config(chunks, wmax, &G, &CPL, &ns);
+  a.items = p->items;
+  a.part = p->part;
+  a.n_items = p->n_items;
+  a.ld_h = ld_h;
+  a.ld_z = ld_z;
+  a.ld_part = ld_h;
+  a.chunks = chunks;
+  a.slab = G * CPL;
+  if (p->n_items == 0) return DG_OK;
+  LaunchFn fn = acc ? pick_launch<true>(G, CPL) : pick_launch<false>(G, CPL);
+  if (!fn) return set_err(DG_ERR_ARG, "dg_spmm_run: no kernel for config");
+  fn(a, ns, S(stream));
+  DG_LAUNCHED();
+  if (p->n_fix) {
+    FixArgs fa;
+    std::memset(&fa, 0, sizeof(fa));
+    for (int r = 0; r < p->n_ranks; ++r) fa.z[r] = z[r];
+    fa.fix = p->fix;
+    fa.part = p->part;
+    fa.ld_z = ld_z;
+    fa.ld_part = ld_h;
+    fa.nfloat = chunks * 4;
+    spmm_fixup_kernel<<<(unsigned)p->n_fix, 128, 0, S(stream)>>>(fa);
+    DG_LAUNCHED();
+  }
+  return DG_OK;
+}
+
+}  // extern "C"
