@@ -220,114 +220,124 @@ def spmm_bytes(vp, rank, f):
     return 4 * (m + 1) + 8 * nnz + 4 * f * u + 4 * f * m, u, nnz, m
 
 
+def _timed(fn, reps, w):
+    """Device time of `reps` calls of fn (CUDA events on the current stream),
+    bracketed by host barrier + synchronize; max over processes."""
+    import torch
+    torch.cuda.synchronize()
+    w.host_barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    w.host_barrier()
+    ms = e0.elapsed_time(e1) / reps
+    return max(w.all_gather_object(ms))
+
+
 def run_ours(args, wl):
     import torch
     import paper_2504_04673_b200 as P
     from paper_2504_04673_b200 import _lib
-    from paper_2504_04673_b200.gcn import GcnRun
-    from paper_2504_04673_b200.spmm import device_plan
+    from paper_2504_04673_b200.dist import world
     from paper_2504_04673_b200.engine import pad4
+    from paper_2504_04673_b200.gcn import GcnRun
+    from paper_2504_04673_b200.plan import build_variant_plan
+    from paper_2504_04673_b200.spmm import device_plan
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
-        raise SystemExit("multi-process bench not built yet")
-    torch.cuda.set_device(0)
+    w = world().init()
+    if w.size != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={w.size}")
+    lead = w.proc == 0
     t_setup = time.time()
     a_hat = make_graph(args.workload)
     n = a_hat.n_rows
     x, y, mask = make_inputs(wl, n)
-    p = args.gpus
+    p = args.gpus * args.ranks_per_gpu
     cfg = P.TrainConfig(layers=wl["layers"], hidden=wl["hidden"], lr=0.01, epochs=1, seed=1,
                         variant=args.variant)
     gr = GcnRun(a_hat, x, y, mask, cfg, p=p, c=1)
-    log(f"[bench] setup {time.time() - t_setup:.1f}s")
+    log(f"[bench] proc {w.proc}: setup {time.time() - t_setup:.1f}s")
     dims = gr.dims
+    grid = gr.grid
 
     # ---- warm-up + timed epochs (inputs resident in HBM; H of layer 1 is
     #      563 MB > 126 MB L2, so no explicit flush is needed) -------------
     gr.run(args.warmup)
     torch.cuda.synchronize()
+    w.host_barrier()
     l0 = _lib.launch_count()
-    clk = ClockSampler(0)
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    ev0.record()
-    run = gr.run(args.steps)
-    ev1.record()
-    torch.cuda.synchronize()
+    clk = ClockSampler(torch.cuda.current_device())
+    holder = {}
+    ms_epoch = _timed(lambda: holder.__setitem__("run", gr.run(args.steps)), 1, w) / args.steps
     clocks = clk.stop()
     launches = _lib.launch_count() - l0
-    ms_total = ev0.elapsed_time(ev1)
-    ms_epoch = ms_total / args.steps
-    res = gr.result(run, args.steps)
+    res = gr.result(holder["run"], args.steps)
 
     # ---- dominant kernel: the f_in-wide forward SpMM of layer 1 ---------
-    dp = device_plan(gr.dm.fwd, gr.grid, args.variant)
+    dp = device_plan(gr.dm.fwd, grid, args.variant)
     f0, ld0 = dims[0], pad4(dims[0])
-    hs = {r: gr.x[gr.dm.boundaries[gr.grid.coords(r)[0]][0]:
-                 gr.dm.boundaries[gr.grid.coords(r)[0]][1]] for r in dp.local}
-    for _ in range(2):
-        dp.run(hs, f0, ld0)
-    reps = 5
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
-    for _ in range(reps):
-        dp.run(hs, f0, ld0)
-    e1.record()
-    torch.cuda.synchronize()
-    t_spmm = e0.elapsed_time(e1) / reps / 1e3
-    tot_b, u_tot, nnz_tot = 0, 0, 0
-    gather_b = 0
+    hs = {r: gr.x[gr.dm.boundaries[grid.coords(r)[0]][0]:
+                 gr.dm.boundaries[grid.coords(r)[0]][1]] for r in dp.local}
+    zs = {r: torch.empty_like(hs[r]) for r in dp.local}
+    dp.exchange_only(hs, f0, ld0)
+    dp.spmm_only(hs, f0, ld0, zs)
+    t_spmm = _timed(lambda: dp.spmm_only(hs, f0, ld0, zs), 3, w) / 1e3
+    t_xchg = _timed(lambda: dp.exchange_only(hs, f0, ld0), 3, w) / 1e3 if p > 1 else None
+    tot_b, gather_b = 0, 0
     for r in dp.local:
         b, u, nnz, m = spmm_bytes(dp.vplan, r, f0)
         tot_b += b
-        u_tot += u
-        nnz_tot += nnz
         gather_b += 4 * (m + 1) + 8 * nnz + 4 * f0 * nnz + 4 * f0 * m
     peak, peak_src = peaks()
     achieved = tot_b / t_spmm / 1e9
 
     # ---- all SpMM phases of one epoch (HBM GB/s over the epoch's SpMMs) --
-    spmm_bytes_epoch = 0
-    for f in dims[:-1] + dims[1:]:
-        for r in dp.local:
-            spmm_bytes_epoch += spmm_bytes(dp.vplan, r, f)[0]
+    widths = dims[:-1] + dims[1:]
+    spmm_bytes_epoch = sum(spmm_bytes(dp.vplan, r, f)[0] for f in widths for r in dp.local)
+    spmm_bytes_epoch = sum(w.all_gather_object(spmm_bytes_epoch))
 
     # ---- communication volume per epoch: aware vs oblivious (elements) --
-    from paper_2504_04673_b200.plan import build_variant_plan
-    widths = dims[:-1] + dims[1:]
-    vp_a = build_variant_plan(gr.dm.fwd, gr.grid, "1d-sparse")
-    vp_o = build_variant_plan(gr.dm.fwd, gr.grid, "1d-oblivious")
+    vp_a = build_variant_plan(gr.dm.fwd, grid, "1d-sparse", [])
+    vp_o = build_variant_plan(gr.dm.fwd, grid, "1d-oblivious", [])
     aware = sum(vp_a.elements(f) for f in widths)
     obl = sum(vp_o.elements(f) for f in widths)
+    exch = None
+    if t_xchg is not None:
+        snd, rcv = dp.traffic_rows()
+        inter = max(max(snd), max(rcv)) * 4 * f0          # wire bytes, busiest rank
+        exch = {"bound": "nvlink", "achieved": round(inter / t_xchg / 1e9, 1),
+                "peak": 770.0, "unit": "GB/s", "frac": round(inter / t_xchg / 1e9 / 770.0, 4),
+                "peak_source": "B200_PROFILING.md measured peer copy per direction",
+                "exchange_ms": round(t_xchg * 1e3, 3), "busiest_rank_bytes": int(inter),
+                "f": f0}
 
     # ---- end to end through the public API with host buffers ------------
-    xh = torch.empty_like(gr.x, device="cpu").pin_memory()
-    xh.copy_(gr.x.cpu())
+    rows = [gr.dm.boundaries[grid.coords(r)[0]] for r in dp.local]
+    xh = {r: gr.x[r0:r1].cpu().pin_memory() for r, (r0, r1) in zip(dp.local, rows)}
     e2e_steps = max(1, min(args.steps, 5))
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    g0.record()
-    d2h = 0
-    for _ in range(e2e_steps):
-        gr.x.copy_(xh, non_blocking=True)
+    d2h = [0]
+
+    def e2e_step():
+        for r, (r0, r1) in zip(dp.local, rows):
+            gr.x[r0:r1].copy_(xh[r], non_blocking=True)
         rr = gr.run(1)
-        st = rr.results[0]["stats"].cpu()      # loss / correct back to the host
-        d2h += st.numel() * st.element_size()
-    g1.record()
-    torch.cuda.synchronize()
-    e2e_ms = g0.elapsed_time(g1) / e2e_steps
-    h2d = gr.x.numel() * 4
+        st = rr.results[grid.rank_of(0, 0)]["stats"].cpu()   # loss / correct to host
+        d2h[0] += st.numel() * st.element_size()
+
+    e2e_ms = _timed(e2e_step, e2e_steps, w)
+    h2d = sum(w.all_gather_object(sum(v.numel() * 4 for v in xh.values())))
 
     # ---- CPU baseline (rank 0, N=1 only) --------------------------------
     cpu = None
-    if not args.no_cpu_baseline:
+    if lead and args.gpus == 1 and not args.no_cpu_baseline:
         cms, rates, sample = cpu_reference_epoch_ms(a_hat, wl, budget_s=args.ref_budget)
         cpu = {"value": round(cms, 1), "unit": "ms", "cores": 1, "kind": "port",
                "sample": sample}
-
+    if not lead:
+        return 0
     line = {
         "metric": "gcn_epoch_ms", "value": round(ms_epoch, 3), "unit": "ms",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -335,21 +345,22 @@ def run_ours(args, wl):
         "vs_baseline": None, "dtype": "f32 (SpMM accumulates f64)", "data": "synthetic",
         "config": {"workload": wl["desc"], "variant": args.variant, "p": p, "c": 1,
                    "partition": "block", "l2": "inputs larger than L2 (H0 = 563 MB)",
-                   "ranks_per_gpu": p // args.gpus},
+                   "ranks_per_gpu": args.ranks_per_gpu},
         "spmm_hbm_gbs": round(spmm_bytes_epoch / (ms_epoch / 1e3) / 1e9, 1),
         "comm_elements_per_epoch": {"aware": int(aware), "oblivious": int(obl),
-                                    "ratio": (aware / obl) if obl else None},
+                                    "ratio": round(aware / obl, 4) if obl else None},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
-                     "kernel": "spmm_rows_kernel (layer-1 forward SpMM, f=%d)" % f0,
+                     "kernel": "spmm_kernel (layer-1 forward SpMM, f=%d, rank 0)" % f0,
                      "algorithmic_bytes": int(tot_b), "kernel_ms": round(t_spmm * 1e3, 3),
                      "gather_gbs": round(gather_b / t_spmm / 1e9, 1), "peak_source": peak_src},
+        "exchange": exch,
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": int(h2d),
-                "d2h_bytes_per_step": int(d2h // e2e_steps)},
+                "d2h_bytes_per_step": int(d2h[0] // e2e_steps)},
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
         "clocks": clocks,
-        "loss": [round(x, 6) for x in res.losses.tolist()],
+        "loss": [round(v, 6) for v in res.losses.tolist()],
         "nnz": int(a_hat.nnz),
     }
     print(json.dumps(line), flush=True)
@@ -366,6 +377,7 @@ def main():
     ap.add_argument("--variant", default="1d-sparse")
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ranks-per-gpu", type=int, default=1)
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":

@@ -94,11 +94,11 @@ int dg_xchg_run(dg_xchg_plan* plan, const float* const* h_src, int n_src,
                 void* stream);
 
 /* ---- group all-reduce: replaces Comm.all_reduce_sum (runtime.py:437-466).
- * For elements [lo, hi): s = src[0] + src[1] + ... (ascending member order,
- * the reference's order), stored to every dst[m].  Each element is reduced
- * exactly once, so all members receive bit-identical values.  Pointers may
- * be peer-mapped; each member reduces its own slice.                      */
-int dg_group_reduce(int g, const float* const* src, float* const* dst, int64_t lo,
+ * For elements [lo, hi): s = src[0] + src[1] + ... + src[g-1] (ascending
+ * member order, the reference's order), stored to dst[0..n_dst).  Every
+ * member that reduces the same range in the same order gets bit-identical
+ * values.  Sources may be peer-mapped (CUDA IPC / P2P over NVLink).       */
+int dg_group_reduce(int g, const float* const* src, int n_dst, float* const* dst, int64_t lo,
                     int64_t hi, int32_t fence_sys, void* stream);
 
 /* ---- cross-process barrier over peer-mapped flag words (device-side;

@@ -165,6 +165,7 @@ struct RArgs {
   float* dst[DG_MAX_GROUP];
   int64_t lo, hi;
   int32_t g;
+  int32_t nd;
   int32_t vec;         // all pointers 16 B aligned and lo % 4 == 0
   int32_t fence_sys;
 };
@@ -185,14 +186,14 @@ __global__ void __launch_bounds__(256) group_reduce_kernel(const __grid_constant
         s.z += x.z;
         s.w += x.w;
       }
-      for (int m = 0; m < a.g; ++m) *reinterpret_cast<float4*>(a.dst[m] + e) = s;
+      for (int m = 0; m < a.nd; ++m) *reinterpret_cast<float4*>(a.dst[m] + e) = s;
     }
     tail = a.lo + 4 * n4;
   }
   for (int64_t e = tail + t0; e < a.hi; e += stride) {
     float s = a.src[0][e];
     for (int m = 1; m < a.g; ++m) s += a.src[m][e];
-    for (int m = 0; m < a.g; ++m) a.dst[m][e] = s;
+    for (int m = 0; m < a.nd; ++m) a.dst[m][e] = s;
   }
   if (a.fence_sys) __threadfence_system();
 }
@@ -240,18 +241,23 @@ __global__ void barrier_kernel(const __grid_constant__ BArgs a) {
 
 extern "C" {
 
-int dg_group_reduce(int g, const float* const* src, float* const* dst, int64_t lo, int64_t hi,
-                    int32_t fence_sys, void* stream) {
-  if (g < 1 || g > DG_MAX_GROUP || hi < lo) return set_err(DG_ERR_ARG, "group_reduce: bad args");
+int dg_group_reduce(int g, const float* const* src, int n_dst, float* const* dst, int64_t lo,
+                    int64_t hi, int32_t fence_sys, void* stream) {
+  if (g < 1 || g > DG_MAX_GROUP || n_dst < 1 || n_dst > DG_MAX_GROUP || hi < lo)
+    return set_err(DG_ERR_ARG, "group_reduce: bad args");
   if (hi == lo) return DG_OK;
   RArgs a;
   std::memset(&a, 0, sizeof(a));
   bool aligned = (lo & 3) == 0;
   for (int m = 0; m < g; ++m) {
     a.src[m] = src[m];
-    a.dst[m] = dst[m];
-    aligned = aligned && (((uintptr_t)src[m] | (uintptr_t)dst[m]) & 15) == 0;
+    aligned = aligned && ((uintptr_t)src[m] & 15) == 0;
   }
+  for (int m = 0; m < n_dst; ++m) {
+    a.dst[m] = dst[m];
+    aligned = aligned && ((uintptr_t)dst[m] & 15) == 0;
+  }
+  a.nd = n_dst;
   a.lo = lo;
   a.hi = hi;
   a.g = g;

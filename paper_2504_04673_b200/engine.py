@@ -63,12 +63,23 @@ def _stream():
 
 
 class DevicePlan:
-    """Device state of one `plan.VariantPlan` for the locally hosted ranks."""
+    """Device state of one `plan.VariantPlan` for the ranks this process
+    hosts.
 
-    def __init__(self, vplan, local_ranks=None, acc=ACC_FP64, max_chunk=MAX_CHUNK):
+    Single process: halo / partial buffers are torch tensors (growable).
+    Multi-process: they are symmetric CUDA-IPC buffers (`dist.SymBuffer`),
+    double-buffered by call parity so a phase never overwrites rows a slow
+    peer is still reading from the previous phase; one device barrier
+    separates the exchange from the SpMM (and, for 1.5D, the SpMM from the
+    row-group reduction)."""
+
+    def __init__(self, vplan, local_ranks=None, acc=ACC_FP64, max_chunk=MAX_CHUNK, max_ld=None):
+        from .dist import world
         lib = L.lib()
         self.vplan = vplan
         self.grid = vplan.grid
+        self.world = world()
+        self.multi = self.world.multi
         self.local = list(range(vplan.grid.p)) if local_ranks is None else list(local_ranks)
         self.li = {r: k for k, r in enumerate(self.local)}
         self.acc = acc
@@ -85,9 +96,9 @@ class DevicePlan:
                                         L.i64_array([x.col_ext.size for x in ro]),
                                         rp, ce, va, max_chunk))
         self._splan = h
+        self._keep = None
         segs = [s for s in vplan.segments if s.src in self.li and s.count > 0]
         self._segs = segs
-        idx_keep = [s.idx for s in segs]
         xh = C.c_void_p()
         L.check(lib.dg_xchg_plan_create(
             C.byref(xh), len(segs), L.i32_array([self.li[s.src] for s in segs]),
@@ -96,14 +107,48 @@ class DevicePlan:
                                                for s in segs]),
             L.i64_array([0] * len(segs)), L.i32_array([s.dst for s in segs]),
             L.i64_array([s.dst_row0 for s in segs])))
-        del idx_keep
         self._xplan = xh
+        self.one_d = vplan.variant.startswith("1d")
+        self.reduce = (not self.one_d) and self.grid.c > 1
         self.halo = {r: None for r in self.local}
         self.partial = {r: None for r in self.local}
-        self.one_d = vplan.variant.startswith("1d")
+        self.parity = 0
         info = (C.c_int64 * 8)()
         L.check(lib.dg_spmm_plan_info(self._splan, info))
         self.info = list(info)
+        if self.multi:
+            self._init_symmetric(max_ld)
+
+    # ---- multi-process symmetric buffers --------------------------------
+    def _init_symmetric(self, max_ld):
+        from .dist import SymBuffer
+        if max_ld is None:
+            raise ValueError("multi-process plans need max_ld up front (IPC buffers are fixed)")
+        self.max_ld = int(max_ld)
+        w, p = self.world, self.grid.p
+        ranks = self.vplan.ranks
+        # per process: its hosted ranks' slots laid out in rank order, two
+        # parities each; every process computes every offset identically
+        self._hoff, self._poff = {}, {}
+        hsize, psize = [0] * w.size, [0] * w.size
+        for r in range(p):
+            q = w.proc_of(r, p)
+            self._hoff[r] = hsize[q]
+            hsize[q] += 2 * ranks[r].halo_rows * self.max_ld * 4
+            self._poff[r] = psize[q]
+            psize[q] += 2 * ranks[r].n_rows * self.max_ld * 4 if self.reduce else 0
+        self.hsym = SymBuffer(w, max(hsize[w.proc], 16))
+        self.psym = SymBuffer(w, max(psize[w.proc], 16)) if self.reduce else None
+
+    def _halo_ptr(self, r, par):
+        q = self.world.proc_of(r, self.grid.p)
+        return (self.hsym.ptrs[q] + self._hoff[r]
+                + par * self.vplan.ranks[r].halo_rows * self.max_ld * 4)
+
+    def _partial_ptr(self, r, par):
+        q = self.world.proc_of(r, self.grid.p)
+        return (self.psym.ptrs[q] + self._poff[r]
+                + par * self.vplan.ranks[r].n_rows * self.max_ld * 4)
 
     def __del__(self):
         try:
@@ -129,32 +174,144 @@ class DevicePlan:
         lib = L.lib()
         st = _stream()
         vp = self.vplan
-        halos = {r: self._buffer(self.halo, r, vp.ranks[r].halo_rows, ld) for r in self.local}
-        if self._segs:
-            dst = [0] * self.grid.p
-            for r in self.local:
-                dst[r] = halos[r].data_ptr()
-            L.check(lib.dg_xchg_run(self._xplan, L.ptr_array([hs[r] for r in self.local]),
-                                    len(self.local), L.ptr_array(dst), len(dst), f, ld, 0, st))
+        p = self.grid.p
         if out is None:
             out = {r: torch.empty((vp.ranks[r].n_rows, ld), dtype=torch.float32,
                                   device=self.device) for r in self.local}
-        if self.one_d or self.grid.c == 1:
-            z = out
+        if self.multi:
+            if ld > self.max_ld:
+                raise ValueError(f"row pitch {ld} exceeds the registered maximum {self.max_ld}")
+            par = self.parity
+            self.parity ^= 1
+            dst = [self._halo_ptr(d, par) for d in range(p)]
+            halo_ptrs = [self._halo_ptr(r, par) for r in self.local]
         else:
-            z = {r: self._buffer(self.partial, r, vp.ranks[r].n_rows, ld) for r in self.local}
+            halos = {r: self._buffer(self.halo, r, vp.ranks[r].halo_rows, ld)
+                     for r in self.local}
+            dst = [0] * p
+            for r in self.local:
+                dst[r] = halos[r].data_ptr()
+            halo_ptrs = [halos[r].data_ptr() for r in self.local]
+        if self._segs:
+            L.check(lib.dg_xchg_run(self._xplan, L.ptr_array([hs[r] for r in self.local]),
+                                    len(self.local), L.ptr_array(dst), len(dst), f, ld,
+                                    1 if self.multi else 0, st))
+        if self.multi:
+            self.world.barrier()            # every peer's rows have landed
+        if not self.reduce:
+            zp = [out[r].data_ptr() for r in self.local]
+        elif self.multi:
+            zp = [self._partial_ptr(r, par) for r in self.local]
+        else:
+            zp = [self._buffer(self.partial, r, vp.ranks[r].n_rows, ld).data_ptr()
+                  for r in self.local]
         L.check(lib.dg_spmm_run(self._splan, L.ptr_array([hs[r] for r in self.local]),
-                                L.ptr_array([halos[r] for r in self.local]),
-                                L.ptr_array([z[r] for r in self.local]), f, ld, ld, self.acc, 0,
+                                L.ptr_array(halo_ptrs), L.ptr_array(zp), f, ld, ld, self.acc, 0,
                                 st))
-        if not self.one_d and self.grid.c > 1:
-            for i in range(self.grid.n_rows):
-                grp = self.grid.row_group(i)
-                if not all(r in self.li for r in grp):
-                    raise NotImplementedError("row group split across processes")
-                n = vp.ranks[grp[0]].n_rows * ld
-                L.check(lib.dg_group_reduce(len(grp), L.ptr_array([z[r] for r in grp]),
-                                            L.ptr_array([out[r] for r in grp]), 0, n, 0, st))
+        if self.reduce:
+            if self.multi:
+                self.world.barrier()        # every replica's partial product is ready
+                for r in self.local:
+                    i, _ = self.grid.coords(r)
+                    grp = self.grid.row_group(i)
+                    n = vp.ranks[r].n_rows * ld
+                    L.check(lib.dg_group_reduce(len(grp), L.ptr_array(
+                        [self._partial_ptr(m, par) for m in grp]), 1, L.ptr_array([out[r]]), 0,
+                        n, 0, st))
+            else:
+                zl = dict(zip(self.local, zp))
+                for i in range(self.grid.n_rows):
+                    grp = self.grid.row_group(i)
+                    n = vp.ranks[grp[0]].n_rows * ld
+                    L.check(lib.dg_group_reduce(len(grp), L.ptr_array([zl[r] for r in grp]),
+                                                len(grp), L.ptr_array([out[r] for r in grp]), 0,
+                                                n, 0, st))
+        return out
+
+    # ---- pieces of a phase, for per-kernel timing in bench.py ------------
+    def exchange_only(self, hs: dict, f: int, ld: int):
+        """The halo exchange of one phase (+ the device barrier that makes
+        the rows visible), without the SpMM."""
+        lib = L.lib()
+        p = self.grid.p
+        if self.multi:
+            par = self.parity
+            dst = [self._halo_ptr(d, par) for d in range(p)]
+        else:
+            dst = [0] * p
+            for r in self.local:
+                dst[r] = self._buffer(self.halo, r, self.vplan.ranks[r].halo_rows,
+                                      ld).data_ptr()
+        if self._segs:
+            L.check(lib.dg_xchg_run(self._xplan, L.ptr_array([hs[r] for r in self.local]),
+                                    len(self.local), L.ptr_array(dst), len(dst), f, ld,
+                                    1 if self.multi else 0, _stream()))
+        if self.multi:
+            self.world.barrier()
+
+    def spmm_only(self, hs: dict, f: int, ld: int, out: dict):
+        """The local SpMM of one phase over the current halo contents."""
+        lib = L.lib()
+        if self.multi:
+            halo_ptrs = [self._halo_ptr(r, self.parity) for r in self.local]
+        else:
+            halo_ptrs = [self._buffer(self.halo, r, self.vplan.ranks[r].halo_rows,
+                                      ld).data_ptr() for r in self.local]
+        L.check(lib.dg_spmm_run(self._splan, L.ptr_array([hs[r] for r in self.local]),
+                                L.ptr_array(halo_ptrs), L.ptr_array([out[r] for r in self.local]),
+                                f, ld, ld, self.acc, 0, _stream()))
+
+    def traffic_rows(self):
+        """(rows sent, rows received) per rank in one phase."""
+        p = self.grid.p
+        snd, rcv = [0] * p, [0] * p
+        for sg in self.vplan.segments:
+            snd[sg.src] += sg.count
+            rcv[sg.dst] += sg.count
+        return snd, rcv
+
+
+class GroupReducer:
+    """Cross-process `all_reduce_sum` for small tensors (the GCN weight
+    gradients): every hosted rank copies its buffer into a symmetric slot,
+    one device barrier, then each rank sums its group's slots (ascending
+    member order, peer-mapped reads) -- bit-identical on every member."""
+
+    def __init__(self, p, numel):
+        from .dist import SymBuffer, world
+        self.w = world()
+        self.p = p
+        self.numel = int(numel)
+        self.slot = (self.numel * 4 + 255) // 256 * 256
+        counts = [0] * self.w.size
+        self.idx = {}
+        for r in range(p):
+            q = self.w.proc_of(r, p)
+            self.idx[r] = counts[q]
+            counts[q] += 1
+        self.sym = SymBuffer(self.w, max(2 * counts[self.w.proc] * self.slot, 16))
+        self.parity = 0
+
+    def _ptr(self, r, par):
+        q = self.w.proc_of(r, self.p)
+        per_par = sum(1 for x in range(self.p) if self.w.proc_of(x, self.p) == q) * self.slot
+        return self.sym.ptrs[q] + par * per_par + self.idx[r] * self.slot
+
+    def __call__(self, bufs: dict, groups: dict) -> dict:
+        from .dist import _as_tensor
+        lib = L.lib()
+        par = self.parity
+        self.parity ^= 1
+        for r, b in bufs.items():
+            _as_tensor(self._ptr(r, par), self.numel, torch.float32).copy_(b.reshape(-1))
+        self.w.barrier()
+        out = {}
+        for r, b in bufs.items():
+            grp = groups[r]
+            o = torch.empty_like(b)
+            L.check(lib.dg_group_reduce(len(grp), L.ptr_array([self._ptr(m, par) for m in grp]),
+                                        1, L.ptr_array([o]), 0, self.numel, 0, _stream()))
+            out[r] = o
         return out
 
 
@@ -171,8 +328,8 @@ def reduce_members(tensors):
             src.append(torch.from_numpy(np.ascontiguousarray(t, dtype=np.float32)).to(dev))
     outs = [torch.empty_like(src[0]) for _ in src]
     n = src[0].numel()
-    L.check(lib.dg_group_reduce(len(src), L.ptr_array(src), L.ptr_array(outs), 0, n, 0,
-                                _stream()))
+    L.check(lib.dg_group_reduce(len(src), L.ptr_array(src), len(outs), L.ptr_array(outs), 0, n,
+                                0, _stream()))
     res = []
     for t, o in zip(tensors, outs):
         res.append(o if isinstance(t, torch.Tensor) else o.double().cpu().numpy())

@@ -218,6 +218,8 @@ class GcnRun:
     def __init__(self, a_hat: CsrMatrix, features, labels, train_mask, cfg: TrainConfig, p=1,
                  c=1, partition=None):
         validate_variant_grid(cfg.variant, p, c)
+        from .dist import world
+        world().init()
         labels, mask = _check_train_inputs(features, labels, train_mask)
         if a_hat.n_rows != features.shape[0]:
             raise ValueError("feature rows must match the matrix")
@@ -255,6 +257,11 @@ class GcnRun:
         self.labels = torch.from_numpy(lab2.astype(np.int64)).to(dev)
         self.mask = torch.from_numpy(msk2.astype(np.uint8)).to(dev)
         self.xent = {}
+        # register the device plans up front (multi-process: fixed IPC
+        # buffers sized for the widest layer)
+        from .spmm import device_plan
+        for op in {id(self.dm.fwd): self.dm.fwd, id(self.dm.bwd): self.dm.bwd}.values():
+            device_plan(op, grid, cfg.variant, max_ld=max(self.lds))
 
     def program(self, comm, epochs, stats, weights_out=None):
         """The per-rank epoch loop (gcn.py:258-286)."""
@@ -307,8 +314,11 @@ class GcnRun:
     def run(self, epochs=None):
         epochs = self.cfg.epochs if epochs is None else epochs
         p = self.grid.p
+        from .dist import world
+        w = world()
+        hosted = w.local_ranks(p) if w.multi else range(p)
         stats = {r: torch.zeros((max(epochs, 1), 2), dtype=torch.float64, device=self.device)
-                 for r in range(p)}
+                 for r in hosted}
         return run_program(p, self.grid.c, lambda comm: self.program(comm, epochs,
                                                                      stats[comm.rank]))
 

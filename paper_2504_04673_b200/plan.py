@@ -198,8 +198,13 @@ def stage_band(grid: ProcessGrid, j):
     return list(range(j * s, (j + 1) * s))
 
 
-def build_variant_plan(op: DistOperand, grid: ProcessGrid, variant: str) -> VariantPlan:
+def build_variant_plan(op: DistOperand, grid: ProcessGrid, variant: str,
+                       local_ranks=None) -> VariantPlan:
+    """Plan of `variant` on `grid`.  The halo layout and exchange segments
+    are computed for every rank (every process needs its peers' offsets);
+    the remapped CSR only for `local_ranks` (default: all)."""
     validate_variant_grid(variant, grid.p, grid.c)
+    hosted = set(range(grid.p)) if local_ranks is None else set(local_ranks)
     aware = variant.endswith("sparse")
     one_d = variant.startswith("1d")
     nb = op.n_blocks
@@ -223,6 +228,9 @@ def build_variant_plan(op: DistOperand, grid: ProcessGrid, variant: str) -> Vari
                 continue
             halo_off[q] = off
             off += cnt
+        if r not in hosted:
+            ranks.append(RankOperand(r, i, j, r1 - r0, r1 - r0, None, None, None, off, halo_off))
+            continue
         local_rows = row_all[lo:hi] - r0
         cols = mat.col_idx[lo:hi]
         vals = mat.values[lo:hi]

@@ -47,13 +47,20 @@ def exchange_index_lists(comm: Comm, op: DistOperand, variant: str):
     comm._collective(("idx", id(op), variant), tuple(range(comm.p)), None, complete)
 
 
-def device_plan(op: DistOperand, grid: ProcessGrid, variant: str, local_ranks=None):
-    """Device plan of `op` for `variant`, built once and cached on the operand."""
-    key = (variant, grid.p, grid.c, torch.cuda.current_device(),
-           None if local_ranks is None else tuple(local_ranks))
+def device_plan(op: DistOperand, grid: ProcessGrid, variant: str, max_ld=None):
+    """Device plan of `op` for `variant` covering the ranks this process
+    hosts (all of them in a single-process run), built once and cached on
+    the operand.  Multi-process plans register fixed-size IPC buffers, so
+    they need the widest row pitch of the run (`max_ld`) up front."""
+    from .dist import world
+    w = world().init()
+    local = w.local_ranks(grid.p) if w.multi else None
+    key = (variant, grid.p, grid.c, torch.cuda.current_device())
     dp = op._device.get(key)
+    if dp is not None and w.multi and max_ld is not None and max_ld > dp.max_ld:
+        raise ValueError(f"row pitch {max_ld} exceeds this plan's registered {dp.max_ld}")
     if dp is None:
-        dp = DevicePlan(build_variant_plan(op, grid, variant), local_ranks)
+        dp = DevicePlan(build_variant_plan(op, grid, variant, local), local, max_ld=max_ld)
         op._device[key] = dp
     return dp
 
@@ -68,7 +75,7 @@ def spmm_phase(comm: Comm, op: DistOperand, h_pad: torch.Tensor, f: int, variant
     ld = pad4(f)
 
     def complete(arr):
-        dp = device_plan(op, grid, variant)
+        dp = device_plan(op, grid, variant, max_ld=ld)
         hs = {}
         for r, h in arr.items():
             hs[r] = h if (isinstance(h, torch.Tensor) and h.dtype == torch.float32
@@ -118,6 +125,8 @@ def run_spmm(a: CsrMatrix, h, p, c, variant, partition=None, index_setup=True) -
     validate_variant_grid(variant, p, c)
     if a.n_rows != a.n_cols:
         raise ValueError("distributed multiply requires a square matrix")
+    from .dist import world
+    world().init()
     numpy_in = not isinstance(h, torch.Tensor)
     if numpy_in:
         h = np.asarray(h, dtype=np.float64)
@@ -138,7 +147,9 @@ def run_spmm(a: CsrMatrix, h, p, c, variant, partition=None, index_setup=True) -
         return spmm_phase(comm, dm.fwd, hd[r0:r1], f, variant)
 
     run: RunResult = run_program(p, c, program)
-    z2 = torch.cat([run.results[grid.rank_of(i, 0)] for i in range(grid.n_rows)], 0)[:, :f]
+    dev = hd.device
+    z2 = torch.cat([run.results[grid.rank_of(i, 0)].to(dev) for i in range(grid.n_rows)],
+                   0)[:, :f]
     if not part.is_identity:
         z2 = z2[torch.from_numpy(part.perm).to(z2.device)]
     z = z2.double().cpu().numpy() if numpy_in else z2

@@ -1,0 +1,86 @@
+"""Run under torchrun (one process per GPU): the multi-process CUDA path
+against the reference's golden vectors.  Exits non-zero on any mismatch.
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/mp_gpu_worker.py
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import paper_2504_04673_b200 as P  # noqa: E402
+from conftest import Golden  # noqa: E402
+from paper_2504_04673_b200.dist import world  # noqa: E402
+
+
+def part_of(g, key, n, k):
+    asg = g[key + "__assign"] if k > 1 else np.zeros(n, np.int64)
+    sizes = np.bincount(asg, minlength=k)
+    bounds, pos = [], 0
+    for s in sizes:
+        bounds.append((pos, pos + int(s)))
+        pos += int(s)
+    return P.Partition(n, k, asg, g[key + "__perm"], bounds)
+
+
+def main():
+    w = world().init()
+    fails = []
+    g = Golden("spmm_golden.npz")
+    n_checked = 0
+    for key in g.cases():
+        a = g.csr(key + "__a", P.CsrMatrix)
+        p, c, vi = (int(x) for x in g[key + "__cfg"])
+        if p < w.size:
+            continue
+        variant = P.VARIANTS[vi]
+        part = part_of(g, key, a.n_rows, p // c)
+        run = P.run_spmm(a, g[key + "__h"], p, c, variant, partition=part)
+        err = np.abs(run.z - g[key + "__z"])
+        if not np.all(err <= 1e-5 * g[key + "__absz"] + 1e-30):
+            fails.append((key, "values", float(err.max())))
+        for (prim, name), ref in g.ledger_fields(key).items():
+            if not np.array_equal(run.ledger.counters[prim][name], ref):
+                fails.append((key, prim, name))
+        fam = "1d" if variant.startswith("1d") else "15d"
+        other = P.run_spmm(a, g[key + "__h"], p, c,
+                           f"{fam}-{'oblivious' if variant.endswith('sparse') else 'sparse'}",
+                           partition=part)
+        if not np.array_equal(other.z, run.z):
+            fails.append((key, "aware != oblivious bitwise"))
+        n_checked += 1
+    gg = Golden("gcn_golden.npz")
+    for key in gg.cases():
+        a = gg.csr(key + "__a", P.CsrMatrix)
+        p, c, layers, hidden, epochs, seed, vi = (int(x) for x in gg[key + "__cfg"])
+        variant = (P.VARIANTS + ("serial",))[vi]
+        if variant == "serial" or p < w.size:
+            continue
+        cfg = P.TrainConfig(layers=layers, hidden=hidden, lr=float(gg[key + "__lr"][0]),
+                            epochs=epochs, seed=seed, variant=variant)
+        part = part_of(gg, key, a.n_rows, p // c) if p // c > 1 else None
+        res = P.train(a, gg[key + "__x"], gg[key + "__y"], gg[key + "__mask"], cfg, p=p, c=c,
+                      partition=part)
+        if not np.allclose(res.losses, gg[key + "__loss"], rtol=1e-5, atol=0):
+            fails.append((key, "loss", res.losses.tolist()))
+        for (prim, name), ref in gg.ledger_fields(key).items():
+            if not np.array_equal(res.ledger.counters[prim][name], ref):
+                fails.append((key, "gcn ledger", prim, name))
+        for per_rank in res.weights_per_rank[1:]:
+            for w0, wr in zip(res.weights_per_rank[0], per_rank):
+                if not np.array_equal(w0, wr):
+                    fails.append((key, "replication"))
+        n_checked += 1
+    print(f"[proc {w.proc}/{w.size}] checked {n_checked} cases, {len(fails)} failures",
+          flush=True)
+    for f in fails:
+        print("FAIL", f, flush=True)
+    sys.exit(1 if fails else 0)
+
+
+if __name__ == "__main__":
+    main()
