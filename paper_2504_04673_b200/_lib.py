@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdgb200.so")
+# DG_LIB_PATH: alternative build (tuning experiments only)
+LIB_PATH = os.environ.get("DG_LIB_PATH", os.path.join(_HERE, "libdgb200.so"))
 
 DG_MAX_LOCAL = 64
 DG_MAX_GROUP = 64

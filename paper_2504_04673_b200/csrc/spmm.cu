@@ -82,9 +82,19 @@ __device__ __forceinline__ int4 ld_stream(const int4* p, uint64_t pol) {
 
 __device__ __forceinline__ float4 ld_h(const float4* p) { return __ldg(p); }
 
+// Occupancy vs in-flight loads (measured on B200, Reddit-shaped graph):
+// one float4 chunk per lane -> 4 entries per step and >= 4 CTAs/SM (<= 64
+// registers); wider lanes keep more registers and fewer CTAs (no spills).
+template <int CPL>
+struct Tune {
+  static constexpr int E = 4;                       // entries per pipeline step
+  static constexpr int MINB = CPL == 1 ? 4 : (CPL == 2 ? 2 : 1);
+};
+
 template <int G, int CPL, bool F64>
-__global__ void __launch_bounds__(256) spmm_kernel(const __grid_constant__ SpmmArgs a) {
-  constexpr int E = (CPL == 1) ? 8 : 4;     // entries per pipeline step
+__global__ void __launch_bounds__(256, Tune<CPL>::MINB)
+    spmm_kernel(const __grid_constant__ SpmmArgs a) {
+  constexpr int E = Tune<CPL>::E;           // entries per pipeline step
   constexpr int E4 = E / 2;                 // int4 loads per step
   const int lig = threadIdx.x & (G - 1);
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -453,10 +463,10 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   if (slab_floats > 0) {
     wmax = std::max(1, slab_floats / 4);
   } else {
-    // one slab of every gathered row within ~2x the 126 MB L2: measured on
-    // B200 (Reddit-shaped, f=602) fewer, wider slabs beat strict L2
-    // residency -- each slab pass re-streams the CSR and re-walks the items
-    const double budget = 256.0 * 1024 * 1024;
+    // one slab of every gathered row within ~half of the 126 MB L2
+    // (measured on B200, Reddit-shaped f=602 with 128-B rows: 64-float slabs
+    // that stay L2-resident beat fewer, wider slabs that spill to DRAM)
+    const double budget = 64.0 * 1024 * 1024;
     const double per_chunk = (double)std::max<int64_t>(ext_total, 1) * 16.0;
     wmax = (int)std::max(1.0, budget / per_chunk);
   }

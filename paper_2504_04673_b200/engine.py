@@ -37,7 +37,11 @@ MAX_CHUNK = 1024      # nonzeros per work item before a row is split
 
 
 def pad4(f: int) -> int:
-    return (int(f) + 3) // 4 * 4
+    """Row pitch (floats) of an f-wide dense operand: 16-byte rows, and
+    128-byte (cache-line) rows for wide layers (f > 64) so a feature slab
+    of a multiple of 32 floats maps onto whole L2 lines."""
+    f = int(f)
+    return (f + 31) // 32 * 32 if f > 64 else (f + 3) // 4 * 4
 
 
 def to_device(h, ld=None, device=None) -> torch.Tensor:

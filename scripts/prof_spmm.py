@@ -27,6 +27,9 @@ def main():
     ap.add_argument("--acc", type=int, nargs="+", default=[1])
     ap.add_argument("--slab", type=int, nargs="+", default=[0])
     ap.add_argument("--chunk", type=int, default=0)
+    ap.add_argument("--ld-align", type=int, default=0)
+    ap.add_argument("--cusparse", action="store_true",
+                    help="also time torch.sparse.mm (cuSPARSE) on the same matrix (comparator)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     a = bench.make_graph(args.workload)
@@ -38,7 +41,7 @@ def main():
     dp = device_plan(dm.fwd, grid, "1d-sparse")
     lib = L.lib()
     for f in args.f:
-        ld = pad4(f)
+        ld = pad4(f) if args.ld_align == 0 else (f + args.ld_align - 1) // args.ld_align * args.ld_align
         h = torch.randn((a.n_rows, ld), device="cuda")
         h[:, f:] = 0
         z = torch.empty_like(h)
@@ -62,6 +65,27 @@ def main():
                 print(f"f={f} slab={slab} acc={acc} chunk={args.chunk}: {t:.3f} ms  "
                       f"gather {gather / t / 1e6:.0f} GB/s  nnz*f/s {a.nnz * f / t / 1e6:.3g} G",
                       flush=True)
+        if args.cusparse:
+            import numpy as np
+            sp = torch.sparse_csr_tensor(torch.from_numpy(a.row_ptr), torch.from_numpy(a.col_idx),
+                                         torch.from_numpy(a.values.astype(np.float32)),
+                                         size=(a.n_rows, a.n_cols), device="cuda")
+            hd = h[:, :f].contiguous()
+            torch.sparse.mm(sp, hd)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.reps):
+                zc = torch.sparse.mm(sp, hd)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / args.reps
+            ref = z[:, :f]
+            rel = float(((zc - ref).abs().max() / ref.abs().max()).item())
+            print(f"f={f} cuSPARSE (torch.sparse.mm fp32): {t:.3f} ms  max rel diff vs ours {rel:.2e}",
+                  flush=True)
+            del sp
 
 
 if __name__ == "__main__":
