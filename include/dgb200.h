@@ -126,6 +126,13 @@ int dg_relu_grad_mul(float* g, int64_t ld_g, const float* zprev, int64_t ld_z,
 /* w -= lr * y  (n contiguous floats) */
 int dg_sgd(float* w, const float* y, int64_t n, float lr, void* stream);
 
+/* ---- diagnostic: random-row gather bandwidth probe (the practical ceiling
+ *      of the SpMM's H-row gathers; used by scripts/gather_roofline.py).
+ *      `groups` groups of `lanes` lanes each sum `per_group` rows tab[idx[k]]
+ *      of 16*lanes bytes.                                                  */
+int dg_diag_gather(const float* tab, int64_t ld, const int32_t* idx, int64_t n_idx,
+                   int32_t lanes, int64_t groups, int32_t per_group, float* out, void* stream);
+
 /* ---- host preprocessing: stable O(nnz + n) transpose, bit-identical to
  *      sparse.transpose_csr (sparse.py:237-247).  Host pointers.          */
 int dg_host_transpose(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,

@@ -291,3 +291,56 @@ int dg_barrier(uint64_t* const* flags, int n_procs, int me, uint64_t epoch, int6
 
 }  // extern "C"
 
+
+// ---------------------------------------------------------------------------
+// diagnostic: random-row gather bandwidth (the practical ceiling of the SpMM's
+// H-row gathers).  Each group of G lanes sums `per_group` rows of `row_bytes`
+// (= 16*G) chosen by idx[]; the table has `rows` rows of pitch `ld` floats.
+// ---------------------------------------------------------------------------
+
+namespace {
+
+template <int G>
+__global__ void __launch_bounds__(256) gather_probe_kernel(const float* __restrict__ tab,
+                                                           int64_t ld, const int32_t* __restrict__ idx,
+                                                           int64_t n_idx, int per_group,
+                                                           float* __restrict__ out) {
+  const int lig = threadIdx.x & (G - 1);
+  const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t base = grp * per_group;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int k = 0; k < per_group; k += 4) {
+    int r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = __ldg(idx + ((base + k + u) % n_idx));
+    float4 x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      x[u] = __ldg(reinterpret_cast<const float4*>(tab + (int64_t)r[u] * ld) + lig);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc.x += x[u].x;
+      acc.y += x[u].y;
+      acc.z += x[u].z;
+      acc.w += x[u].w;
+    }
+  }
+  if (acc.x == 123.456f) out[0] = acc.y + acc.z + acc.w;   // keep the loads alive
+}
+
+}  // namespace
+
+extern "C" int dg_diag_gather(const float* tab, int64_t ld, const int32_t* idx, int64_t n_idx,
+                              int32_t lanes, int64_t groups, int32_t per_group, float* out,
+                              void* stream) {
+  const unsigned blocks = (unsigned)((groups * lanes + 255) / 256);
+  switch (lanes) {
+    case 4: gather_probe_kernel<4><<<blocks, 256, 0, S(stream)>>>(tab, ld, idx, n_idx, per_group, out); break;
+    case 8: gather_probe_kernel<8><<<blocks, 256, 0, S(stream)>>>(tab, ld, idx, n_idx, per_group, out); break;
+    case 16: gather_probe_kernel<16><<<blocks, 256, 0, S(stream)>>>(tab, ld, idx, n_idx, per_group, out); break;
+    case 32: gather_probe_kernel<32><<<blocks, 256, 0, S(stream)>>>(tab, ld, idx, n_idx, per_group, out); break;
+    default: return set_err(DG_ERR_ARG, "diag_gather: lanes must be 4, 8, 16 or 32");
+  }
+  DG_LAUNCHED();
+  return DG_OK;
+}
