@@ -42,6 +42,11 @@ WORKLOADS = {
     "rmat14": dict(desc="R-MAT scale 14 (Graph500 .57/.19/.19, edge factor 16), f=16, "
                         "2-layer GCN (layers=3, hidden=16), C=16",
                    n=16_384, f_in=16, classes=16, layers=3, hidden=16),
+    "products": dict(desc="ogbn-products-shaped planted-partition power-law graph (2,449,029 "
+                          "vertices, 123,718,280 stored off-diagonal nonzeros + self-loops, 256 "
+                          "hidden communities), f_in=100, 3-layer GCN (layers=4, hidden=16), C=47, "
+                          "community-preserving partition",
+                     n=2_449_029, f_in=100, classes=47, layers=4, hidden=16),
 }
 
 
@@ -58,12 +63,17 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
+_COMM = {}
+
+
 def make_graph(name, seed=0):
     import paper_2504_04673_b200 as P
     from paper_2504_04673_b200 import graphgen
     t = time.time()
     if name == "reddit":
         a = graphgen.reddit_shaped_device(seed=seed)
+    elif name == "products":
+        a, _COMM["products"] = graphgen.products_shaped_device(seed=seed)
     else:
         a = graphgen.rmat(14, 16, seed)
     log(f"[bench] graph {name}: n={a.n_rows} nnz={a.nnz} ({time.time() - t:.1f}s)")
@@ -187,7 +197,8 @@ def run_reference(args, wl):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": wl["desc"], "variant": "1d-sparse", "p": args.gpus, "c": 1},
+        "config": {"workload": wl["desc"], "variant": args.variant,
+                   "p": args.gpus * args.ranks_per_gpu, "c": args.c},
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": 1, "kind": "port",
                          "sample": sample,
                          "rates_nnz_f_per_s": {str(k): round(v) for k, v in rates.items()}},
@@ -256,9 +267,16 @@ def run_ours(args, wl):
     n = a_hat.n_rows
     x, y, mask = make_inputs(wl, n)
     p = args.gpus * args.ranks_per_gpu
+    c = args.c
     cfg = P.TrainConfig(layers=wl["layers"], hidden=wl["hidden"], lr=0.01, epochs=1, seed=1,
                         variant=args.variant)
-    gr = GcnRun(a_hat, x, y, mask, cfg, p=p, c=1)
+    part = None
+    part_name = "block"
+    if args.workload in _COMM and p // c > 1:
+        from paper_2504_04673_b200.graphgen import community_partition
+        part = community_partition(_COMM[args.workload], p // c)
+        part_name = "planted-community (stand-in for METIS/GVB)"
+    gr = GcnRun(a_hat, x, y, mask, cfg, p=p, c=c, partition=part)
     log(f"[bench] proc {w.proc}: setup {time.time() - t_setup:.1f}s")
     dims = gr.dims
     grid = gr.grid
@@ -300,14 +318,22 @@ def run_ours(args, wl):
     spmm_bytes_epoch = sum(w.all_gather_object(spmm_bytes_epoch))
 
     # ---- communication volume per epoch: aware vs oblivious (elements) --
-    vp_a = build_variant_plan(gr.dm.fwd, grid, "1d-sparse", [])
-    vp_o = build_variant_plan(gr.dm.fwd, grid, "1d-oblivious", [])
+    fam = "1d" if args.variant.startswith("1d") else "15d"
+    vp_a = build_variant_plan(gr.dm.fwd, grid, f"{fam}-sparse", [])
+    vp_o = build_variant_plan(gr.dm.fwd, grid, f"{fam}-oblivious", [])
     aware = sum(vp_a.elements(f) for f in widths)
     obl = sum(vp_o.elements(f) for f in widths)
     exch = None
     if t_xchg is not None:
-        snd, rcv = dp.traffic_rows()
-        inter = max(max(snd), max(rcv)) * 4 * f0          # wire bytes, busiest rank
+        # NVLink bytes only (segments between ranks on different GPUs), per
+        # GPU; the busiest GPU's max(send, receive) sets the exchange time
+        snd, rcv = [0] * w.size, [0] * w.size
+        for sg in dp.vplan.segments:
+            qs, qd = w.proc_of(sg.src, p), w.proc_of(sg.dst, p)
+            if qs != qd:
+                snd[qs] += sg.count
+                rcv[qd] += sg.count
+        inter = max(max(snd), max(rcv)) * 4 * f0
         exch = {"bound": "nvlink", "achieved": round(inter / t_xchg / 1e9, 1),
                 "peak": 770.0, "unit": "GB/s", "frac": round(inter / t_xchg / 1e9 / 770.0, 4),
                 "peak_source": "B200_PROFILING.md measured peer copy per direction",
@@ -343,8 +369,9 @@ def run_ours(args, wl):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_epoch, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 (SpMM accumulates f64)", "data": "synthetic",
-        "config": {"workload": wl["desc"], "variant": args.variant, "p": p, "c": 1,
-                   "partition": "block", "l2": "inputs larger than L2 (H0 = 563 MB)",
+        "config": {"workload": wl["desc"], "variant": args.variant, "p": p, "c": c,
+                   "partition": part_name,
+                   "l2": "inputs larger than L2 (H0 = %d MB)" % (gr.x.numel() * 4 // 2**20),
                    "ranks_per_gpu": args.ranks_per_gpu},
         "spmm_hbm_gbs": round(spmm_bytes_epoch / (ms_epoch / 1e3) / 1e9, 1),
         "comm_elements_per_epoch": {"aware": int(aware), "oblivious": int(obl),
@@ -378,6 +405,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ranks-per-gpu", type=int, default=1)
+    ap.add_argument("--c", type=int, default=1, help="1.5D replication factor")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":

@@ -139,6 +139,12 @@ int dg_host_transpose(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
                       const int64_t* col, const double* val, int64_t* out_row_ptr,
                       int64_t* out_col, double* out_val);
 
+/* ---- host preprocessing: symmetric permutation P A P^T (new id perm[i]),
+ *      equal to partition.apply_partition (partition.py:231-254).          */
+int dg_host_permute(int64_t n, const int64_t* row_ptr, const int64_t* col, const double* val,
+                    const int64_t* perm, int64_t* out_row_ptr, int64_t* out_col,
+                    double* out_val);
+
 #ifdef __cplusplus
 }
 #endif

@@ -113,3 +113,43 @@ extern "C" int dg_host_transpose(int64_t n_rows, int64_t n_cols, const int64_t* 
   return DG_OK;
 }
 
+
+// ---------------------------------------------------------------------------
+// host preprocessing (native): symmetric permutation P A P^T
+// (partition.apply_partition, partition.py:231-254: new ids perm[], entries
+// ordered by (new row, new col) -- the (row, col) keys are unique, so the
+// result equals the reference's lexsort exactly)
+// ---------------------------------------------------------------------------
+
+extern "C" int dg_host_permute(int64_t n, const int64_t* row_ptr, const int64_t* col,
+                               const double* val, const int64_t* perm, int64_t* out_row_ptr,
+                               int64_t* out_col, double* out_val) {
+  if (n < 0) return set_err(DG_ERR_ARG, "permute: bad n");
+  std::vector<int64_t> inv(n);
+  for (int64_t i = 0; i < n; ++i) {
+    if (perm[i] < 0 || perm[i] >= n) return set_err(DG_ERR_ARG, "permute: perm out of range");
+    inv[perm[i]] = i;
+  }
+  out_row_ptr[0] = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t o = inv[r];
+    out_row_ptr[r + 1] = out_row_ptr[r] + (row_ptr[o + 1] - row_ptr[o]);
+  }
+  std::vector<std::pair<int64_t, double>> tmp;
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t o = inv[r];
+    const int64_t lo = row_ptr[o], len = row_ptr[o + 1] - lo;
+    tmp.resize(len);
+    for (int64_t k = 0; k < len; ++k) tmp[k] = {perm[col[lo + k]], val[lo + k]};
+    std::sort(tmp.begin(), tmp.end(),
+              [](const std::pair<int64_t, double>& a, const std::pair<int64_t, double>& b) {
+                return a.first < b.first;
+              });
+    const int64_t d = out_row_ptr[r];
+    for (int64_t k = 0; k < len; ++k) {
+      out_col[d + k] = tmp[k].first;
+      out_val[d + k] = tmp[k].second;
+    }
+  }
+  return DG_OK;
+}

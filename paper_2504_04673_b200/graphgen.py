@@ -166,7 +166,8 @@ def sbm(n, blocks=2, p_in=0.2, p_out=0.01, seed=0, feature_dim=16, feature_scale
 # large shaped graphs, generated on the GPU (benchmark input synthesis)
 # ---------------------------------------------------------------------------
 
-def chung_lu_device(n, pairs, alpha=0.6, max_weight=None, seed=0, communities=0, p_in=0.8):
+def chung_lu_device(n, pairs, alpha=0.6, max_weight=None, seed=0, communities=0, p_in=0.8,
+                    return_communities=False):
     """Power-law (Chung-Lu) symmetric 0/1 graph with exactly `pairs`
     undirected edges, sampled on the GPU with torch (input synthesis only).
 
@@ -231,9 +232,10 @@ def chung_lu_device(n, pairs, alpha=0.6, max_weight=None, seed=0, communities=0,
     rp[1:] = torch.cumsum(torch.bincount(rows, minlength=n), 0)
     out = CsrMatrix(n, n, rp.cpu().numpy(), cols.cpu().numpy(), np.ones(cols.numel()),
                     check=False)
+    comm_host = comm.cpu().numpy() if communities else None
     del keys, rows, cols, key2, rp
     torch.cuda.empty_cache()
-    return out
+    return (out, comm_host) if return_communities else out
 
 
 def reddit_shaped_device(seed=0, n=232_965, nnz=114_848_856):
@@ -245,6 +247,24 @@ def reddit_shaped_device(seed=0, n=232_965, nnz=114_848_856):
 
 def products_shaped_device(seed=0, n=2_449_029, nnz=2 * 61_859_140, communities=256):
     """Config 3/4 graph on the GPU: 2.45M vertices, 123.7M stored
-    off-diagonal nonzeros, power-law degrees inside hidden communities."""
+    off-diagonal nonzeros, power-law degrees inside hidden communities.
+    Returns (adjacency, planted community of every vertex)."""
     return chung_lu_device(n, nnz // 2, alpha=0.55, max_weight=17_481, seed=seed,
-                           communities=communities, p_in=0.8)
+                           communities=communities, p_in=0.8, return_communities=True)
+
+
+def community_partition(communities, k):
+    """k-way partition that keeps planted communities whole, balanced by
+    vertex count (largest community first onto the lightest part) -- the
+    stand-in for the paper's METIS / GVB reordering on the products-shaped
+    graph (the reference's Python partitioners take hours at 2.4M vertices)."""
+    from .partition import Partition
+    comm = np.asarray(communities, dtype=np.int64)
+    sizes = np.bincount(comm)
+    load = np.zeros(k, dtype=np.int64)
+    part_of_comm = np.zeros(sizes.size, dtype=np.int64)
+    for c in np.argsort(-sizes, kind="stable"):
+        t = int(np.argmin(load))
+        part_of_comm[c] = t
+        load[t] += sizes[c]
+    return Partition.from_assignment(part_of_comm[comm], k)

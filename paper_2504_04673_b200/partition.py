@@ -203,14 +203,18 @@ def apply_partition(a: CsrMatrix, h, part: Partition):
             raise ValueError("row count of h must match the matrix")
     if part.is_identity:
         return a, h
-    perm = part.perm
-    nr = perm[a.row_of_nnz()]
-    nc = perm[a.col_idx]
-    order = np.lexsort((nc, nr))
+    from . import _lib as L
+    perm = np.ascontiguousarray(part.perm, dtype=np.int64)
     rp = np.zeros(a.n_rows + 1, dtype=np.int64)
-    if a.nnz:
-        np.cumsum(np.bincount(nr, minlength=a.n_rows), out=rp[1:])
-    a2 = CsrMatrix(a.n_rows, a.n_cols, rp, nc[order], a.values[order], check=False)
+    ci = np.empty(a.nnz, dtype=np.int64)
+    va = np.empty(a.nnz, dtype=np.float64)
+    src = [np.ascontiguousarray(x) for x in (a.row_ptr, a.col_idx, a.values)]
+    rc = L.host_lib().dg_host_permute(a.n_rows, src[0].ctypes.data, src[1].ctypes.data,
+                                      src[2].ctypes.data, perm.ctypes.data, rp.ctypes.data,
+                                      ci.ctypes.data, va.ctypes.data)
+    if rc != 0:
+        raise ValueError(L.host_lib().dg_last_error().decode())
+    a2 = CsrMatrix(a.n_rows, a.n_cols, rp, ci, va, check=False)
     h2 = None if h is None else h[part.inv_perm]
     return a2, h2
 
