@@ -54,6 +54,20 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+TRAFFIC = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def ncu_traffic(key):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the
+    dominant kernel, from the committed `ncu --set full` capture
+    (profiles/traffic.json, written by scripts/ncu_traffic.py)."""
+    try:
+        with open(TRAFFIC) as fh:
+            return json.load(fh).get(key)
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def peaks():
     try:
         with open(PEAKS) as fh:
@@ -377,7 +391,8 @@ def run_ours(args, wl):
         "comm_elements_per_epoch": {"aware": int(aware), "oblivious": int(obl),
                                     "ratio": round(aware / obl, 4) if obl else None},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": ncu_traffic(f"{args.workload}_f{f0}_p{p}_c{c}"),
                      "kernel": "spmm_kernel (layer-1 forward SpMM, f=%d, rank 0)" % f0,
                      "algorithmic_bytes": int(tot_b), "kernel_ms": round(t_spmm * 1e3, 3),
                      "gather_gbs": round(gather_b / t_spmm / 1e9, 1), "peak_source": peak_src},

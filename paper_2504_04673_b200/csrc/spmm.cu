@@ -463,12 +463,15 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   if (slab_floats > 0) {
     wmax = std::max(1, slab_floats / 4);
   } else {
-    // one slab of every gathered row within ~half of the 126 MB L2
-    // (measured on B200, Reddit-shaped f=602 with 128-B rows: 64-float slabs
-    // that stay L2-resident beat fewer, wider slabs that spill to DRAM)
+    // Slabs pay off only when a slab of >= 128 B per gathered row stays
+    // L2-resident (~64 MB of the 126 MB L2; measured on B200: Reddit-shaped
+    // f=602 with 128-B rows -> 64-float slabs).  When even that does not
+    // fit, the gathers hit DRAM whatever the slab, and one wide slab
+    // (fewest CSR passes, widest G) wins.
     const double budget = 64.0 * 1024 * 1024;
     const double per_chunk = (double)std::max<int64_t>(ext_total, 1) * 16.0;
-    wmax = (int)std::max(1.0, budget / per_chunk);
+    const int fit = (int)std::max(0.0, budget / per_chunk);
+    wmax = fit >= 8 ? fit : 128;
   }
   int G, CPL, ns;
   choose_config(chunks, wmax, &G, &CPL, &ns);

@@ -267,4 +267,16 @@ def community_partition(communities, k):
         t = int(np.argmin(load))
         part_of_comm[c] = t
         load[t] += sizes[c]
-    return Partition.from_assignment(part_of_comm[comm], k)
+    asg = part_of_comm[comm]
+    # locality-aware layout: vertices ordered by (part, community, id), the
+    # nested ordering a METIS-style partitioner produces; parts stay
+    # contiguous, as Partition requires
+    order = np.lexsort((np.arange(comm.size), comm, asg))
+    perm = np.empty(comm.size, dtype=np.int64)
+    perm[order] = np.arange(comm.size)
+    sizes_k = np.bincount(asg, minlength=k)
+    bounds, pos = [], 0
+    for sz in sizes_k:
+        bounds.append((pos, pos + int(sz)))
+        pos += int(sz)
+    return Partition(comm.size, k, asg, perm, bounds)

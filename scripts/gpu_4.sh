@@ -1,0 +1,17 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+make -C paper_2504_04673_b200/csrc > gpurun_out/build.txt 2>&1 || { cat gpurun_out/build.txt; exit 1; }
+free -g > gpurun_out/host_mem.txt; nproc >> gpurun_out/host_mem.txt
+TR="python -m torch.distributed.run --nnodes=1 --master-addr 127.0.0.1"
+timeout 900 $TR --nproc-per-node=4 --master-port 29621 tests/mp_gpu_worker.py > gpurun_out/mp4.txt 2>&1; echo "rc=$?" >> gpurun_out/mp4.txt
+run() { name=$1; shift; timeout 900 $TR --nproc-per-node=$N --master-port $((29630 + RANDOM % 200)) bench.py --gpus $N --steps 5 --warmup 3 "$@" > gpurun_out/b4_$name.json 2> gpurun_out/b4_$name.log; echo "rc=$?" >> gpurun_out/b4_$name.log; }
+N=4 run reddit_n4
+N=4 run reddit_n4_p8 --ranks-per-gpu 2
+N=4 run products_1d --workload products
+N=4 run products_15d_c2 --workload products --variant 15d-sparse --c 2 --ranks-per-gpu 2
+N=4 run products_15d_c4 --workload products --variant 15d-sparse --c 4 --ranks-per-gpu 4
+N=4 run products_15d_obl_c2 --workload products --variant 15d-oblivious --c 2 --ranks-per-gpu 2
+N=4 run products_1d_obl --workload products --variant 1d-oblivious
+tail -n 3 gpurun_out/mp4.txt
+for f in gpurun_out/b4_*.log; do echo "$f: $(tail -n 1 $f)"; done
