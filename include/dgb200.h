@@ -59,20 +59,23 @@ int dg_ipc_close(void* dev_ptr);
  * Host arrays are copied; long rows are split into fixed chunks of at most
  * `max_chunk` nonzeros and reduced in a fixed order (deterministic).     */
 typedef struct dg_spmm_plan dg_spmm_plan;
+#define DG_PLAN_SKIP_EMPTY_ROWS 1  /* no work items for rows without entries (z untouched) */
 int dg_spmm_plan_create(dg_spmm_plan** plan, int n_ranks,
                         const int64_t* n_rows, const int64_t* n_local, const int64_t* nnz,
                         const int64_t* const* row_ptr, const int32_t* const* col_ext,
-                        const float* const* val, int32_t max_chunk);
+                        const float* const* val, int32_t max_chunk, int32_t flags);
 int dg_spmm_plan_destroy(dg_spmm_plan* plan);
 /* info[0]=items, [1]=split rows, [2]=chunks, [3]=total nnz, [4]=device bytes */
 int dg_spmm_plan_info(const dg_spmm_plan* plan, int64_t info[8]);
 /* z[r] (n_rows[r] x ld_z, device) = A_r @ [h_local[r]; h_halo[r]] (ld_h).
  * f <= ld_h, ld_h % 4 == 0, ld_z % 4 == 0.  acc: 0 = fp32 accumulate,
  * 1 = fp64 accumulate.  slab_floats: feature-slab width (0 = auto: sized
- * so one slab of the gathered rows stays L2-resident).                   */
+ * so one slab of the gathered rows stays L2-resident).  beta = 1 adds the
+ * product to z (the halo pass of a phase whose own-block pass overlapped
+ * the exchange).                                                        */
 int dg_spmm_run(dg_spmm_plan* plan, const float* const* h_local, const float* const* h_halo,
                 float* const* z, int32_t f, int64_t ld_h, int64_t ld_z, int32_t acc,
-                int32_t slab_floats, void* stream);
+                int32_t slab_floats, int32_t beta, void* stream);
 
 /* ---- halo exchange: replaces the pack `h_block[NnzCols(dst, me)]`
  *      (spmm.py:185, 212), Comm.all_to_allv / isend / broadcast

@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("DG_LIB_PATH", os.path.join(_HERE, "libdgb200.so"))
 
 DG_MAX_LOCAL = 64
 DG_MAX_GROUP = 64
+DG_PLAN_SKIP_EMPTY_ROWS = 1
 
 _lock = threading.Lock()
 _lib = None
@@ -40,11 +41,11 @@ _SIGS = {
     "dg_ipc_open_handle": (C.c_int, [C.POINTER(C.c_uint8), c_vpp]),
     "dg_ipc_close": (C.c_int, [c_vp]),
     "dg_spmm_plan_create": (C.c_int, [c_vpp, C.c_int, c_i64p, c_i64p, c_i64p, c_vpp, c_vpp,
-                                      c_vpp, C.c_int32]),
+                                      c_vpp, C.c_int32, C.c_int32]),
     "dg_spmm_plan_destroy": (C.c_int, [c_vp]),
     "dg_spmm_plan_info": (C.c_int, [c_vp, c_i64p]),
     "dg_spmm_run": (C.c_int, [c_vp, c_vpp, c_vpp, c_vpp, C.c_int32, C.c_int64, C.c_int64,
-                              C.c_int32, C.c_int32, c_vp]),
+                              C.c_int32, C.c_int32, C.c_int32, c_vp]),
     "dg_xchg_plan_create": (C.c_int, [c_vpp, C.c_int, c_i32p, c_i64p, c_vpp, c_i64p, c_i32p,
                                       c_i64p]),
     "dg_xchg_plan_destroy": (C.c_int, [c_vp]),

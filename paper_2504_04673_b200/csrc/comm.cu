@@ -27,7 +27,11 @@ struct XArgs {
   int32_t fence_sys;
 };
 
-template <int G>
+// One group of G lanes moves one row; lane l owns float4 chunks l, l+G, ...
+// (up to CPL per lane).  All of a lane's loads are issued before its
+// stores, so a warp keeps CPL x 512 B of (possibly remote, NVLink) stores in
+// flight per row instead of one load-store round trip per chunk.
+template <int G, int CPL>
 __global__ void __launch_bounds__(256) xchg_kernel(const __grid_constant__ XArgs a) {
   const XSeg sg = a.segs[blockIdx.y];
   const int lig = threadIdx.x & (G - 1);
@@ -40,7 +44,17 @@ __global__ void __launch_bounds__(256) xchg_kernel(const __grid_constant__ XArgs
     const int64_t srow = sg.idx ? (int64_t)__ldg(sg.idx + k) : sg.src_row0 + k;
     const float4* s = src + srow * ld4;
     float4* d = dst + (sg.dst_row0 + k) * ld4;
-    for (int c = lig; c < a.chunks; c += G) d[c] = __ldg(s + c);
+    float4 v[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int c = lig + q * G;
+      if (c < a.chunks) v[q] = __ldg(s + c);
+    }
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int c = lig + q * G;
+      if (c < a.chunks) d[c] = v[q];
+    }
   }
   if (a.fence_sys) __threadfence_system();
 }
@@ -124,7 +138,7 @@ int dg_xchg_run(dg_xchg_plan* p, const float* const* h_src, int n_src, float* co
   if (!p) return set_err(DG_ERR_ARG, "xchg_run: null plan");
   if (p->n_segs == 0 || p->max_count == 0) return DG_OK;
   if (n_src < p->max_src || n_dst < p->max_dst || n_src > DG_MAX_LOCAL ||
-      n_dst > 2 * DG_MAX_LOCAL * 2 || ld % 4 || f > ld || f < 1)
+      n_dst > 2 * DG_MAX_LOCAL * 2 || ld % 4 || f > ld || f < 1 || (f + 3) / 4 > 512)
     return set_err(DG_ERR_ARG, "xchg_run: bad buffer tables / ld");
   XArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -136,18 +150,33 @@ int dg_xchg_run(dg_xchg_plan* p, const float* const* h_src, int n_src, float* co
   a.fence_sys = fence_sys;
   int G = 1;
   while (G < a.chunks && G < 32) G <<= 1;
+  const int cpl = (a.chunks + G - 1) / G;
   const int64_t per_block = 256 / G;
   int64_t gx = (p->max_count + per_block - 1) / per_block;
-  gx = std::min<int64_t>(std::max<int64_t>(gx, 1), 4 * 148);
+  gx = std::min<int64_t>(std::max<int64_t>(gx, 1), 16 * 148);
   dim3 grid((unsigned)gx, (unsigned)p->n_segs);
-  switch (G) {
-    case 1: xchg_kernel<1><<<grid, 256, 0, S(stream)>>>(a); break;
-    case 2: xchg_kernel<2><<<grid, 256, 0, S(stream)>>>(a); break;
-    case 4: xchg_kernel<4><<<grid, 256, 0, S(stream)>>>(a); break;
-    case 8: xchg_kernel<8><<<grid, 256, 0, S(stream)>>>(a); break;
-    case 16: xchg_kernel<16><<<grid, 256, 0, S(stream)>>>(a); break;
-    default: xchg_kernel<32><<<grid, 256, 0, S(stream)>>>(a); break;
+  cudaStream_t st = S(stream);
+#define DG_X(g, c) xchg_kernel<g, c><<<grid, 256, 0, st>>>(a)
+  if (G < 32) {
+    switch (G) {
+      case 1: DG_X(1, 1); break;
+      case 2: DG_X(2, 1); break;
+      case 4: DG_X(4, 1); break;
+      case 8: DG_X(8, 1); break;
+      default: DG_X(16, 1); break;
+    }
+  } else if (cpl <= 1) {
+    DG_X(32, 1);
+  } else if (cpl <= 2) {
+    DG_X(32, 2);
+  } else if (cpl <= 4) {
+    DG_X(32, 4);
+  } else if (cpl <= 8) {
+    DG_X(32, 8);
+  } else {
+    DG_X(32, 16);
   }
+#undef DG_X
   DG_LAUNCHED();
   return DG_OK;
 }

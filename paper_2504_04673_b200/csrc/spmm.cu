@@ -62,6 +62,7 @@ struct SpmmArgs {
   int64_t ld_part;
   int32_t chunks;      // ceil(f / 4): float4 chunks that carry features
   int32_t slab;        // chunks per slab (= G * CPL)
+  int32_t beta;        // 1: z += result (boundary pass of an overlapped phase)
 };
 
 __device__ __forceinline__ uint64_t evict_first_policy() {
@@ -192,12 +193,27 @@ __global__ void __launch_bounds__(256, Tune<CPL>::MINB)
     for (int q = 0; q < CPL; ++q)
       if (on[q]) {
         float4 o;
+        float4* zq = reinterpret_cast<float4*>(zp) + chk[q];
         if constexpr (F64) {
+          if (a.beta) {
+            const float4 zo = *zq;
+            acc[q][0] += (double)zo.x;
+            acc[q][1] += (double)zo.y;
+            acc[q][2] += (double)zo.z;
+            acc[q][3] += (double)zo.w;
+          }
           o = make_float4((float)acc[q][0], (float)acc[q][1], (float)acc[q][2], (float)acc[q][3]);
         } else {
           o = make_float4(part[q][0], part[q][1], part[q][2], part[q][3]);
+          if (a.beta) {
+            const float4 zo = *zq;
+            o.x += zo.x;
+            o.y += zo.y;
+            o.z += zo.z;
+            o.w += zo.w;
+          }
         }
-        reinterpret_cast<float4*>(zp)[chk[q]] = o;
+        *zq = o;
       }
   } else {
     double* pp = a.part + (int64_t)it.slot * a.ld_part;
@@ -222,6 +238,7 @@ struct FixArgs {
   int64_t ld_z;
   int64_t ld_part;
   int32_t nfloat;      // chunks * 4
+  int32_t beta;
 };
 
 __global__ void __launch_bounds__(128) spmm_fixup_kernel(const __grid_constant__ FixArgs a) {
@@ -230,6 +247,7 @@ __global__ void __launch_bounds__(128) spmm_fixup_kernel(const __grid_constant__
   for (int c = threadIdx.x; c < a.nfloat; c += blockDim.x) {
     double s = 0.0;
     for (int k = 0; k < fx.n; ++k) s += a.part[(int64_t)(fx.slot0 + k) * a.ld_part + c];
+    if (a.beta) s += (double)zp[c];
     zp[c] = (float)s;
   }
 }
@@ -320,7 +338,8 @@ int dg_spmm_plan_destroy(dg_spmm_plan* p) {
 int dg_spmm_plan_create(dg_spmm_plan** out, int n_ranks, const int64_t* n_rows,
                         const int64_t* n_local, const int64_t* nnz,
                         const int64_t* const* row_ptr, const int32_t* const* col_ext,
-                        const float* const* val, int32_t max_chunk) {
+                        const float* const* val, int32_t max_chunk, int32_t flags) {
+  const bool skip_empty = (flags & DG_PLAN_SKIP_EMPTY_ROWS) != 0;
   if (!out || n_ranks < 1 || n_ranks > DG_MAX_LOCAL || max_chunk < 1)
     return set_err(DG_ERR_ARG, "dg_spmm_plan_create: bad args");
   auto* p = new dg_spmm_plan();
@@ -342,6 +361,7 @@ int dg_spmm_plan_create(dg_spmm_plan** out, int n_ranks, const int64_t* n_rows,
     for (int64_t i = 0; i < n_rows[r]; ++i) {
       const int64_t lo = row_ptr[r][i], hi = row_ptr[r][i + 1];
       const int64_t len = hi - lo;
+      if (len == 0 && skip_empty) continue;
       if (len <= max_chunk) {
         items.push_back(Item{lo, (int32_t)i, (int32_t)len, r, -1});
       } else {
@@ -433,7 +453,7 @@ int dg_spmm_plan_info(const dg_spmm_plan* p, int64_t info[8]) {
 
 int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const* h_halo,
                 float* const* z, int32_t f, int64_t ld_h, int64_t ld_z, int32_t acc,
-                int32_t slab_floats, void* stream) {
+                int32_t slab_floats, int32_t beta, void* stream) {
   if (!p) return set_err(DG_ERR_ARG, "dg_spmm_run: null plan");
   if (f < 1 || ld_h % 4 || ld_z % 4 || f > ld_h || f > ld_z)
     return set_err(DG_ERR_ARG, "dg_spmm_run: need 1 <= f <= ld, ld % 4 == 0");
@@ -483,6 +503,7 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   a.ld_part = ld_h;
   a.chunks = chunks;
   a.slab = G * CPL;
+  a.beta = beta ? 1 : 0;
   if (p->n_items == 0) return DG_OK;
   LaunchFn fn = acc ? pick_launch<true>(G, CPL) : pick_launch<false>(G, CPL);
   if (!fn) return set_err(DG_ERR_ARG, "dg_spmm_run: no kernel for config");
@@ -497,6 +518,7 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
     fa.ld_z = ld_z;
     fa.ld_part = ld_h;
     fa.nfloat = chunks * 4;
+    fa.beta = beta ? 1 : 0;
     spmm_fixup_kernel<<<(unsigned)p->n_fix, 128, 0, S(stream)>>>(fa);
     DG_LAUNCHED();
   }

@@ -66,16 +66,49 @@ def _stream():
     return L.stream_ptr()
 
 
+def _make_spmm_plan(rank_ops, max_chunk, flags=0):
+    """dg_spmm_plan over a list of RankOperand-like objects (row_ptr,
+    col_ext, val, n_rows, n_local)."""
+    lib = L.lib()
+    n = len(rank_ops)
+    rp = (C.c_void_p * n)(*[x.row_ptr.ctypes.data for x in rank_ops])
+    ce = (C.c_void_p * n)(*[x.col_ext.ctypes.data for x in rank_ops])
+    va = (C.c_void_p * n)(*[x.val.ctypes.data for x in rank_ops])
+    h = C.c_void_p()
+    L.check(lib.dg_spmm_plan_create(C.byref(h), n, L.i64_array([x.n_rows for x in rank_ops]),
+                                    L.i64_array([x.n_local for x in rank_ops]),
+                                    L.i64_array([x.col_ext.size for x in rank_ops]),
+                                    rp, ce, va, max_chunk, flags))
+    return h
+
+
+class _Part:
+    """A rank operand restricted to its own-block (interior) or halo
+    (boundary) entries, storage order kept."""
+
+    def __init__(self, ro, boundary):
+        keep = (ro.col_ext >= ro.n_local) if boundary else (ro.col_ext < ro.n_local)
+        rows = np.repeat(np.arange(ro.n_rows, dtype=np.int64), np.diff(ro.row_ptr))[keep]
+        self.n_rows, self.n_local = ro.n_rows, ro.n_local
+        self.row_ptr = np.zeros(ro.n_rows + 1, dtype=np.int64)
+        if rows.size:
+            np.cumsum(np.bincount(rows, minlength=ro.n_rows), out=self.row_ptr[1:])
+        self.col_ext = np.ascontiguousarray(ro.col_ext[keep])
+        self.val = np.ascontiguousarray(ro.val[keep])
+
+
 class DevicePlan:
     """Device state of one `plan.VariantPlan` for the ranks this process
     hosts.
 
-    Single process: halo / partial buffers are torch tensors (growable).
-    Multi-process: they are symmetric CUDA-IPC buffers (`dist.SymBuffer`),
+    Single process: halo / partial buffers are torch tensors (growable); a
+    phase is exchange -> SpMM -> (1.5D) group reduction on one stream.
+    Multi-process: buffers are symmetric CUDA-IPC buffers (`dist.SymBuffer`),
     double-buffered by call parity so a phase never overwrites rows a slow
-    peer is still reading from the previous phase; one device barrier
-    separates the exchange from the SpMM (and, for 1.5D, the SpMM from the
-    row-group reduction)."""
+    peer is still reading from the previous phase.  The SpMM is split into
+    an own-block (interior) pass that runs on the main stream while the
+    exchange + device barrier run on a side stream, and a halo (boundary)
+    pass that accumulates into Z once the barrier has passed."""
 
     def __init__(self, vplan, local_ranks=None, acc=ACC_FP64, max_chunk=MAX_CHUNK, max_ld=None):
         from .dist import world
@@ -89,18 +122,15 @@ class DevicePlan:
         self.acc = acc
         self.device = torch.device("cuda", torch.cuda.current_device())
         ro = [vplan.ranks[r] for r in self.local]
-        self._keep = ro
-        n = len(ro)
-        rp = (C.c_void_p * n)(*[x.row_ptr.ctypes.data for x in ro])
-        ce = (C.c_void_p * n)(*[x.col_ext.ctypes.data for x in ro])
-        va = (C.c_void_p * n)(*[x.val.ctypes.data for x in ro])
-        h = C.c_void_p()
-        L.check(lib.dg_spmm_plan_create(C.byref(h), n, L.i64_array([x.n_rows for x in ro]),
-                                        L.i64_array([x.n_local for x in ro]),
-                                        L.i64_array([x.col_ext.size for x in ro]),
-                                        rp, ce, va, max_chunk))
-        self._splan = h
-        self._keep = None
+        self.overlap = self.multi
+        if self.overlap:
+            self._splan = _make_spmm_plan([_Part(x, False) for x in ro], max_chunk)
+            self._bplan = _make_spmm_plan([_Part(x, True) for x in ro], max_chunk,
+                                          L.DG_PLAN_SKIP_EMPTY_ROWS)
+            self._side = torch.cuda.Stream(device=self.device)
+        else:
+            self._splan = _make_spmm_plan(ro, max_chunk)
+            self._bplan = None
         segs = [s for s in vplan.segments if s.src in self.li and s.count > 0]
         self._segs = segs
         xh = C.c_void_p()
@@ -157,8 +187,9 @@ class DevicePlan:
     def __del__(self):
         try:
             lib = L.lib()
-            if getattr(self, "_splan", None):
-                lib.dg_spmm_plan_destroy(self._splan)
+            for h in (getattr(self, "_splan", None), getattr(self, "_bplan", None)):
+                if h:
+                    lib.dg_spmm_plan_destroy(h)
             if getattr(self, "_xplan", None):
                 lib.dg_xchg_plan_destroy(self._xplan)
         except Exception:  # noqa: BLE001 - interpreter teardown
@@ -172,6 +203,17 @@ class DevicePlan:
             store[r] = buf
         return buf[:need].view(rows, ld)
 
+    def _spmm(self, plan, hs, halo_ptrs, zp, f, ld, beta, stream):
+        L.check(L.lib().dg_spmm_run(plan, L.ptr_array([hs[r] for r in self.local]),
+                                    L.ptr_array(halo_ptrs), L.ptr_array(zp), f, ld, ld, self.acc,
+                                    0, beta, stream))
+
+    def _xchg(self, hs, dst, f, ld, stream):
+        if self._segs:
+            L.check(L.lib().dg_xchg_run(self._xplan, L.ptr_array([hs[r] for r in self.local]),
+                                        len(self.local), L.ptr_array(dst), len(dst), f, ld,
+                                        1 if self.multi else 0, stream))
+
     def run(self, hs: dict, f: int, ld: int, out: dict = None) -> dict:
         """One multiply phase.  hs[r]: (n_i, ld) fp32 CUDA tensor for every
         hosted rank r; returns {r: (n_i, ld) tensor}."""
@@ -182,47 +224,21 @@ class DevicePlan:
         if out is None:
             out = {r: torch.empty((vp.ranks[r].n_rows, ld), dtype=torch.float32,
                                   device=self.device) for r in self.local}
-        if self.multi:
-            if ld > self.max_ld:
-                raise ValueError(f"row pitch {ld} exceeds the registered maximum {self.max_ld}")
-            par = self.parity
-            self.parity ^= 1
-            dst = [self._halo_ptr(d, par) for d in range(p)]
-            halo_ptrs = [self._halo_ptr(r, par) for r in self.local]
-        else:
+        if not self.multi:
             halos = {r: self._buffer(self.halo, r, vp.ranks[r].halo_rows, ld)
                      for r in self.local}
             dst = [0] * p
             for r in self.local:
                 dst[r] = halos[r].data_ptr()
-            halo_ptrs = [halos[r].data_ptr() for r in self.local]
-        if self._segs:
-            L.check(lib.dg_xchg_run(self._xplan, L.ptr_array([hs[r] for r in self.local]),
-                                    len(self.local), L.ptr_array(dst), len(dst), f, ld,
-                                    1 if self.multi else 0, st))
-        if self.multi:
-            self.world.barrier()            # every peer's rows have landed
-        if not self.reduce:
-            zp = [out[r].data_ptr() for r in self.local]
-        elif self.multi:
-            zp = [self._partial_ptr(r, par) for r in self.local]
-        else:
-            zp = [self._buffer(self.partial, r, vp.ranks[r].n_rows, ld).data_ptr()
-                  for r in self.local]
-        L.check(lib.dg_spmm_run(self._splan, L.ptr_array([hs[r] for r in self.local]),
-                                L.ptr_array(halo_ptrs), L.ptr_array(zp), f, ld, ld, self.acc, 0,
-                                st))
-        if self.reduce:
-            if self.multi:
-                self.world.barrier()        # every replica's partial product is ready
-                for r in self.local:
-                    i, _ = self.grid.coords(r)
-                    grp = self.grid.row_group(i)
-                    n = vp.ranks[r].n_rows * ld
-                    L.check(lib.dg_group_reduce(len(grp), L.ptr_array(
-                        [self._partial_ptr(m, par) for m in grp]), 1, L.ptr_array([out[r]]), 0,
-                        n, 0, st))
+            self._xchg(hs, dst, f, ld, st)
+            if self.reduce:
+                zp = [self._buffer(self.partial, r, vp.ranks[r].n_rows, ld).data_ptr()
+                      for r in self.local]
             else:
+                zp = [out[r].data_ptr() for r in self.local]
+            self._spmm(self._splan, hs, [halos[r].data_ptr() for r in self.local], zp, f, ld,
+                       0, st)
+            if self.reduce:
                 zl = dict(zip(self.local, zp))
                 for i in range(self.grid.n_rows):
                     grp = self.grid.row_group(i)
@@ -230,13 +246,41 @@ class DevicePlan:
                     L.check(lib.dg_group_reduce(len(grp), L.ptr_array([zl[r] for r in grp]),
                                                 len(grp), L.ptr_array([out[r] for r in grp]), 0,
                                                 n, 0, st))
+            return out
+        # ---- multi-process: overlap the own-block SpMM with the exchange --
+        if ld > self.max_ld:
+            raise ValueError(f"row pitch {ld} exceeds the registered maximum {self.max_ld}")
+        par = self.parity
+        self.parity ^= 1
+        dst = [self._halo_ptr(d, par) for d in range(p)]
+        halo_ptrs = [self._halo_ptr(r, par) for r in self.local]
+        main = torch.cuda.current_stream()
+        self._side.wait_stream(main)                    # H is ready
+        with torch.cuda.stream(self._side):
+            self._xchg(hs, dst, f, ld, L.stream_ptr(self._side))
+            self.world.barrier()                        # every peer's rows have landed
+        zp = ([self._partial_ptr(r, par) for r in self.local] if self.reduce
+              else [out[r].data_ptr() for r in self.local])
+        self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, st)       # own block
+        main.wait_stream(self._side)
+        self._spmm(self._bplan, hs, halo_ptrs, zp, f, ld, 1, st)       # halo rows, z +=
+        for r in self.local:                            # inputs in use on the side stream
+            hs[r].record_stream(self._side)
+        if self.reduce:
+            self.world.barrier()                        # every replica's partial is ready
+            for r in self.local:
+                i, _ = self.grid.coords(r)
+                grp = self.grid.row_group(i)
+                n = vp.ranks[r].n_rows * ld
+                L.check(lib.dg_group_reduce(len(grp), L.ptr_array(
+                    [self._partial_ptr(m, par) for m in grp]), 1, L.ptr_array([out[r]]), 0,
+                    n, 0, st))
         return out
 
     # ---- pieces of a phase, for per-kernel timing in bench.py ------------
     def exchange_only(self, hs: dict, f: int, ld: int):
         """The halo exchange of one phase (+ the device barrier that makes
         the rows visible), without the SpMM."""
-        lib = L.lib()
         p = self.grid.p
         if self.multi:
             par = self.parity
@@ -246,24 +290,22 @@ class DevicePlan:
             for r in self.local:
                 dst[r] = self._buffer(self.halo, r, self.vplan.ranks[r].halo_rows,
                                       ld).data_ptr()
-        if self._segs:
-            L.check(lib.dg_xchg_run(self._xplan, L.ptr_array([hs[r] for r in self.local]),
-                                    len(self.local), L.ptr_array(dst), len(dst), f, ld,
-                                    1 if self.multi else 0, _stream()))
+        self._xchg(hs, dst, f, ld, _stream())
         if self.multi:
             self.world.barrier()
 
     def spmm_only(self, hs: dict, f: int, ld: int, out: dict):
-        """The local SpMM of one phase over the current halo contents."""
-        lib = L.lib()
+        """The local SpMM of one phase (own block + halo) over the current
+        halo contents, no exchange."""
         if self.multi:
             halo_ptrs = [self._halo_ptr(r, self.parity) for r in self.local]
         else:
             halo_ptrs = [self._buffer(self.halo, r, self.vplan.ranks[r].halo_rows,
                                       ld).data_ptr() for r in self.local]
-        L.check(lib.dg_spmm_run(self._splan, L.ptr_array([hs[r] for r in self.local]),
-                                L.ptr_array(halo_ptrs), L.ptr_array([out[r] for r in self.local]),
-                                f, ld, ld, self.acc, 0, _stream()))
+        zp = [out[r].data_ptr() for r in self.local]
+        self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, _stream())
+        if self._bplan is not None:
+            self._spmm(self._bplan, hs, halo_ptrs, zp, f, ld, 1, _stream())
 
     def traffic_rows(self):
         """(rows sent, rows received) per rank in one phase."""

@@ -49,7 +49,7 @@ def main():
             for slab in args.slab:
                 def go():
                     L.check(lib.dg_spmm_run(dp._splan, L.ptr_array([h]), L.ptr_array([h]),
-                                            L.ptr_array([z]), f, ld, ld, acc, slab,
+                                            L.ptr_array([z]), f, ld, ld, acc, slab, 0,
                                             L.stream_ptr()))
                 go()
                 torch.cuda.synchronize()
