@@ -24,7 +24,11 @@ __device__ __forceinline__ int warp_min(int v) {
   return v;
 }
 
-// one warp per row; 8 rows per block; deterministic two-level reduction
+// Masked softmax cross-entropy (gcn.py:98-120).  One warp per row in a
+// grid-stride loop over a fixed grid (<= 4 CTAs per SM), so the cross-CTA
+// reduction touches one counter a few hundred times, not once per 8 rows.
+// Loss / correct sums are deterministic: each warp sums its rows in order,
+// each CTA its warps in order, the last CTA the CTA partials in order.
 __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ x, int64_t n, int C,
                                                    int64_t ld, const int64_t* __restrict__ labels,
                                                    const uint8_t* __restrict__ mask, double denom,
@@ -35,15 +39,14 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ x, 
   __shared__ double s_corr[8];
   __shared__ bool s_last;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * 8 + w;
   double loss = 0.0, corr = 0.0;
-  if (row < n) {
+  for (int64_t row = (int64_t)blockIdx.x * 8 + w; row < n; row += (int64_t)gridDim.x * 8) {
     const float* xr = x + row * ld;
     float m = -INFINITY;
     for (int j = lane; j < C; j += 32) m = fmaxf(m, xr[j]);
     m = warp_max(m);
     double s = 0.0;
-    for (int j = lane; j < C; j += 32) s += exp((double)xr[j] - (double)m);
+    for (int j = lane; j < C; j += 32) s += (double)expf(xr[j] - m);
     s = warp_sum(s);
     int am = C;
     for (int j = lane; j < C; j += 32)
@@ -55,10 +58,11 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ x, 
     const bool on = mask[row] != 0;
     const int64_t lbl = labels[row];
     float* gr = grad + row * ldg;
+    const double inv_s = 1.0 / s;
     for (int j = lane; j < C; j += 32) {
       float gv = 0.f;
       if (on) {
-        double sm = exp((double)xr[j] - (double)m) / s;
+        double sm = (double)expf(xr[j] - m) * inv_s;
         if (j == lbl) sm -= 1.0;
         gv = (float)(sm / denom);
       }
@@ -66,8 +70,8 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ x, 
     }
     for (int j = C + lane; j < ldg; j += 32) gr[j] = 0.f;
     if (on) {
-      loss = log(s) - ((double)xr[lbl] - (double)m);
-      corr = (am == lbl) ? 1.0 : 0.0;
+      loss += log(s) - ((double)xr[lbl] - (double)m);
+      corr += (am == lbl) ? 1.0 : 0.0;
     }
   }
   if (lane == 0) {
@@ -88,30 +92,16 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ x, 
     s_last = (done == gridDim.x - 1);
   }
   __syncthreads();
-  if (s_last) {
+  if (s_last && threadIdx.x == 0) {
     __threadfence();
-    __shared__ double r_l[256];
-    __shared__ double r_c[256];
     double l = 0.0, c = 0.0;
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+    for (unsigned b = 0; b < gridDim.x; ++b) {
       l += ((volatile double*)scratch)[2 * b];
       c += ((volatile double*)scratch)[2 * b + 1];
     }
-    r_l[threadIdx.x] = l;
-    r_c[threadIdx.x] = c;
-    __syncthreads();
-    for (int o = 128; o; o >>= 1) {
-      if ((int)threadIdx.x < o) {
-        r_l[threadIdx.x] += r_l[threadIdx.x + o];
-        r_c[threadIdx.x] += r_c[threadIdx.x + o];
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      out[0] += r_l[0];
-      out[1] += r_c[0];
-      *counter = 0u;
-    }
+    out[0] += l;
+    out[1] += c;
+    *counter = 0u;
   }
 }
 
@@ -157,7 +147,7 @@ int dg_xent(const float* logits, int64_t n, int32_t C, int64_t ld, const int64_t
             const uint8_t* mask, double denom, float* grad, int64_t ld_grad, double* scratch,
             uint32_t* counter, double* stats_out, void* stream) {
   if (n < 1 || C < 1 || C > ld || C > ld_grad) return set_err(DG_ERR_ARG, "xent: bad args");
-  const unsigned blocks = (unsigned)((n + 7) / 8);
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 7) / 8, 4 * 148);
   xent_kernel<<<blocks, 256, 0, S(stream)>>>(logits, n, C, ld, labels, mask, denom, grad,
                                              ld_grad, scratch, counter, stats_out);
   DG_LAUNCHED();

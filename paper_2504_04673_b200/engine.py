@@ -132,6 +132,12 @@ class DevicePlan:
             self._splan = _make_spmm_plan(ro, max_chunk)
             self._bplan = None
         segs = [s for s in vplan.segments if s.src in self.li and s.count > 0]
+        # blocks are dispatched roughly in segment order: rotate every
+        # sender's destinations by process distance so that at any moment
+        # each GPU receives from one sender (no incast on one NVLink ingress)
+        w, p = self.world, vplan.grid.p
+        segs.sort(key=lambda sg: ((w.proc_of(sg.dst, p) - w.proc_of(sg.src, p)) % w.size,
+                                  (sg.dst - sg.src) % p, sg.src))
         self._segs = segs
         xh = C.c_void_p()
         L.check(lib.dg_xchg_plan_create(
