@@ -310,6 +310,13 @@ def run_ours(args, wl):
     launches = _lib.launch_count() - l0
     res = gr.result(holder["run"], args.steps)
 
+    # ---- per-phase breakdown of one extra epoch (CUDA events between steps)
+    from paper_2504_04673_b200.gcn import PhaseTimer
+    gr.timer = PhaseTimer()
+    gr.run(1)
+    breakdown = {k: round(v, 3) for k, v in gr.timer.summary().items()}
+    gr.timer = None
+
     # ---- dominant kernel: the f_in-wide forward SpMM of layer 1 ---------
     dp = device_plan(gr.dm.fwd, grid, args.variant)
     f0, ld0 = dims[0], pad4(dims[0])
@@ -403,6 +410,7 @@ def run_ours(args, wl):
                 "d2h_bytes_per_step": int(d2h[0] // e2e_steps)},
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
+        "epoch_breakdown_ms": breakdown,
         "clocks": clocks,
         "loss": [round(v, 6) for v in res.losses.tolist()],
         "nnz": int(a_hat.nnz),

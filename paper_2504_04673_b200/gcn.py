@@ -208,6 +208,27 @@ def _check_train_inputs(features, labels, train_mask):
     return labels, mask
 
 
+class PhaseTimer:
+    """Optional CUDA-event marks between the steps of an epoch (bench
+    breakdown).  `mark(name)` records an event on the current stream; the
+    time attributed to `name` is the gap since the previous mark."""
+
+    def __init__(self):
+        self.events = []
+
+    def mark(self, name):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.events.append((name, e))
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for (_, e0), (name, e1) in zip(self.events[:-1], self.events[1:]):
+            out[name] = out.get(name, 0.0) + e0.elapsed_time(e1)
+        return out
+
+
 class GcnRun:
     """Device state of one training run (shared by every hosted rank).
 
@@ -257,6 +278,7 @@ class GcnRun:
         self.labels = torch.from_numpy(lab2.astype(np.int64)).to(dev)
         self.mask = torch.from_numpy(msk2.astype(np.uint8)).to(dev)
         self.xent = {}
+        self.timer = None             # PhaseTimer for a breakdown run (bench)
         # register the device plans up front (multi-process: fixed IPC
         # buffers sized for the widest layer)
         from .spmm import device_plan
@@ -280,11 +302,15 @@ class GcnRun:
         lib = L.lib()
         st = L.stream_ptr()
         dims, lds = self.dims, self.lds
+        tm = self.timer if comm.rank == min(comm._rt.local) else None
+        mark = tm.mark if tm is not None else (lambda name: None)
         with _no_tf32():
             for epoch in range(epochs):
+                mark("epoch_start")
                 hs, zs = [h0], []
                 for l, w in enumerate(ws):
                     t = spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant)
+                    mark(f"fwd_spmm_f{dims[l]}")
                     z = torch.mm(t, w)
                     zs.append(z)
                     if l < last:
@@ -294,13 +320,17 @@ class GcnRun:
                         hs.append(h)
                     else:
                         hs.append(z)
+                    mark(f"fwd_dense_{l}")
                 logits = hs[-1]
                 g = torch.empty_like(logits)
                 xent(logits, dims[-1], yb, mb, self.denom, g, stats[epoch])
+                mark("xent")
                 for l in range(last, -1, -1):
                     m = spmm_phase(comm, dm.bwd, g, dims[l + 1], cfg.variant)
+                    mark(f"bwd_spmm_f{dims[l + 1]}")
                     y = comm.all_reduce_sum(torch.mm(hs[l].T, m), group=col_group,
                                             elems=dims[l] * dims[l + 1])
+                    mark(f"bwd_wgrad_{l}")
                     if l > 0:
                         g = torch.mm(m, ws[l].T)
                         L.check(lib.dg_relu_grad_mul(g.data_ptr(), g.stride(0),
@@ -308,6 +338,7 @@ class GcnRun:
                                                      g.shape[0], dims[l], st))
                     L.check(lib.dg_sgd(ws[l].data_ptr(), y.data_ptr(), ws[l].numel(),
                                        float(cfg.lr), st))
+                    mark(f"bwd_dense_{l}")
                 comm.ledger_mark(("epoch", epoch))
         return {"stats": stats, "weights": ws}
 
