@@ -127,7 +127,9 @@ class DevicePlan:
             self._splan = _make_spmm_plan([_Part(x, False) for x in ro], max_chunk)
             self._bplan = _make_spmm_plan([_Part(x, True) for x in ro], max_chunk,
                                           L.DG_PLAN_SKIP_EMPTY_ROWS)
-            self._side = torch.cuda.Stream(device=self.device)
+            # high priority: the exchange's blocks are dispatched ahead of the
+            # own-block SpMM's (otherwise the 10^5-block SpMM grid starves it)
+            self._side = torch.cuda.Stream(device=self.device, priority=-1)
         else:
             self._splan = _make_spmm_plan(ro, max_chunk)
             self._bplan = None
