@@ -129,6 +129,23 @@ int dg_relu_grad_mul(float* g, int64_t ld_g, const float* zprev, int64_t ld_z,
 /* w -= lr * y  (n contiguous floats) */
 int dg_sgd(float* w, const float* y, int64_t n, float lr, void* stream);
 
+/* ---- dense transforms of the GCN step (gcn.py:274-282), fp32 SIMT,
+ *      HBM-bound tall-skinny shapes (cuBLAS picks SIMT kernels ~4x off
+ *      bandwidth for these).
+ * dg_dense_rows: C[r, :] = A[r, :K] @ B (K x N; transB: B is N x K, i.e.
+ *   W^T), N <= 64, K * roundup16(N) <= 16384.  Optional epilogues:
+ *   C_relu = max(C, 0) (gcn.py:276); C *= 1[z_mask > 0] (gcn.py:282).
+ *   Columns [N, ldc) of C are written as zeros.
+ * dg_dense_tn: Y (K x ldy) = H[:, :K]^T @ M[:, :N], reduced over the n rows
+ *   (gcn.py:280), deterministically: per-slice partials in fp64, summed in
+ *   slice order.  work: >= dg_dense_tn_work(n, K, N) doubles.            */
+int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float* B, int64_t ldb,
+                  int32_t N, int32_t transB, float* C, int64_t ldc, float* C_relu,
+                  const float* z_mask, int64_t ld_mask, void* stream);
+int64_t dg_dense_tn_work(int64_t n, int32_t K, int32_t N);
+int dg_dense_tn(const float* H, int64_t ldh, int64_t n, int32_t K, const float* M, int64_t ldm,
+                int32_t N, float* Y, int64_t ldy, double* work, int64_t work_len, void* stream);
+
 /* ---- diagnostic: random-row gather bandwidth probe (the practical ceiling
  *      of the SpMM's H-row gathers; used by scripts/gather_roofline.py).
  *      `groups` groups of `lanes` lanes each sum `per_group` rows tab[idx[k]]

@@ -60,6 +60,11 @@ _SIGS = {
     "dg_relu_grad_mul": (C.c_int, [c_vp, C.c_int64, c_vp, C.c_int64, C.c_int64, C.c_int32,
                                    c_vp]),
     "dg_sgd": (C.c_int, [c_vp, c_vp, C.c_int64, C.c_float, c_vp]),
+    "dg_dense_rows": (C.c_int, [c_vp, C.c_int64, C.c_int64, C.c_int32, c_vp, C.c_int64, C.c_int32,
+                                C.c_int32, c_vp, C.c_int64, c_vp, c_vp, C.c_int64, c_vp]),
+    "dg_dense_tn_work": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
+    "dg_dense_tn": (C.c_int, [c_vp, C.c_int64, C.c_int64, C.c_int32, c_vp, C.c_int64, C.c_int32,
+                              c_vp, C.c_int64, c_vp, C.c_int64, c_vp]),
     "dg_diag_gather": (C.c_int, [c_vp, C.c_int64, c_vp, C.c_int64, C.c_int32, C.c_int64,
                                  C.c_int32, c_vp, c_vp]),
     "dg_host_permute": (C.c_int, [C.c_int64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

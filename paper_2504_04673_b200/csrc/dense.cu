@@ -1,0 +1,277 @@
+// dense.cu -- the GCN's dense transforms, tall-skinny and memory-bound:
+//
+//   forward   Z = T W            gcn.py:274  (T: n x K, W: K x N, N <= 64)
+//             H = relu(Z)        gcn.py:276  (fused epilogue, optional)
+//   backward  G = (M W^T) * 1[Zprev > 0]     gcn.py:282  (fused mask, optional)
+//   wgrad     Y = H^T M          gcn.py:280  (K x N, reduction over the n rows)
+//
+// fp32 SIMT (TF32 would break the fp32 parity contract); these shapes are
+// HBM-bound (T or H is read once: 566 MB for Reddit layer 1), so the target
+// is streaming the tall operand at HBM speed, not tensor-core FLOPs.
+//
+// dg_dense_rows: a CTA owns 64 rows x all N columns; B lives in shared
+// memory (K x N <= 16K floats); A is staged in 32-wide k-chunks, transposed
+// so a thread reads 4 consecutive rows with one 16-B shared load; thread
+// tile 4 rows x N/16 columns.
+//
+// dg_dense_tn: grid = (row slices, 64-wide K blocks); each CTA accumulates
+// its slice's partial H^T M (fp32 per 32-row chunk, folded into fp64) and
+// writes it to `work`; a second kernel sums the partials in slice order
+// (fp64) -- deterministic, unlike split-K with atomics.
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int BM = 64;   // rows per CTA (dense_rows)
+constexpr int BK = 32;   // k-chunk
+
+template <int TN>
+__global__ void __launch_bounds__(256) dense_rows_kernel(
+    const float* __restrict__ A, int64_t lda, int64_t n, int K, const float* __restrict__ B,
+    int64_t ldb, int N, int transB, float* __restrict__ C, int64_t ldc,
+    float* __restrict__ Crelu, const float* __restrict__ Zmask, int64_t ldm) {
+  extern __shared__ float smem[];
+  constexpr int NP = 16 * TN;                       // padded N
+  float* Bs = smem;                                  // K x NP
+  float* As = smem + (size_t)K * NP;                 // BK x (BM + 4)
+  const int tid = threadIdx.x;
+  const int tx = tid % 16;                           // column group
+  const int ty = tid / 16;                           // row group (4 rows)
+  for (int i = tid; i < K * NP; i += 256) {
+    const int k = i / NP, j = i % NP;
+    float b = 0.f;
+    if (j < N) b = transB ? B[(int64_t)j * ldb + k] : B[(int64_t)k * ldb + j];
+    Bs[i] = b;
+  }
+  const int64_t row0 = (int64_t)blockIdx.x * BM;
+  float acc[4][TN];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) acc[r][c] = 0.f;
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    __syncthreads();
+    // stage A[row0:row0+64, k0:k0+32] transposed: As[k][r]
+    for (int i = tid; i < BM * BK / 4; i += 256) {
+      const int r = i / (BK / 4), q = i % (BK / 4);
+      const int64_t gr = row0 + r;
+      const int k = k0 + 4 * q;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gr < n) {
+        const float* ap = A + gr * lda + k;
+        if (k + 3 < K) {
+          v = *reinterpret_cast<const float4*>(ap);
+        } else {
+          if (k < K) v.x = ap[0];
+          if (k + 1 < K) v.y = ap[1];
+          if (k + 2 < K) v.z = ap[2];
+        }
+      }
+      As[(4 * q + 0) * (BM + 4) + r] = v.x;
+      As[(4 * q + 1) * (BM + 4) + r] = v.y;
+      As[(4 * q + 2) * (BM + 4) + r] = v.z;
+      As[(4 * q + 3) * (BM + 4) + r] = v.w;
+    }
+    __syncthreads();
+    const int kmax = min(BK, K - k0);
+    for (int kk = 0; kk < kmax; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[kk * (BM + 4) + 4 * ty]);
+      const float* bp = &Bs[(k0 + kk) * NP + tx * TN];
+      float b[TN];
+#pragma unroll
+      for (int c = 0; c < TN; ++c) b[c] = bp[c];
+#pragma unroll
+      for (int c = 0; c < TN; ++c) {
+        acc[0][c] = fmaf(a.x, b[c], acc[0][c]);
+        acc[1][c] = fmaf(a.y, b[c], acc[1][c]);
+        acc[2][c] = fmaf(a.z, b[c], acc[2][c]);
+        acc[3][c] = fmaf(a.w, b[c], acc[3][c]);
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int64_t gr = row0 + 4 * ty + r;
+    if (gr >= n) continue;
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      const int j = tx * TN + c;
+      if (j >= ldc) continue;
+      float v = acc[r][c];
+      if (Zmask && j < N && !(Zmask[gr * ldm + j] > 0.f)) v = 0.f;
+      C[gr * ldc + j] = v;
+      if (Crelu) Crelu[gr * ldc + j] = fmaxf(v, 0.f);
+    }
+  }
+}
+
+// Y partials: CTA (bx, by) sums rows [bx*rows_per, ...) for K columns
+// [by*64, by*64+64) x all N (<= 64) outputs; thread tile 4 (k) x TN (n).
+template <int TN>
+__global__ void __launch_bounds__(256) dense_tn_kernel(
+    const float* __restrict__ H, int64_t ldh, int64_t n, int K, const float* __restrict__ M,
+    int64_t ldm, int N, int64_t rows_per, double* __restrict__ work) {
+  constexpr int NP = 16 * TN;
+  constexpr int RC = 32;                             // rows per chunk
+  __shared__ __align__(16) float Hs[RC][64 + 4];
+  __shared__ __align__(16) float Ms[RC][NP + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16;                           // n group
+  const int ty = tid / 16;                           // k group (4)
+  const int k0 = blockIdx.y * 64;
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per;
+  const int64_t r_end = min(n, r_begin + rows_per);
+  float part[4][TN];
+  double acc[4][TN];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+      part[i][c] = 0.f;
+      acc[i][c] = 0.0;
+    }
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += RC) {
+    __syncthreads();
+    for (int i = tid; i < RC * 16; i += 256) {       // H chunk: 32 rows x 64 cols
+      const int rr = i / 16, q = i % 16;
+      const int64_t gr = r0 + rr;
+      const int k = k0 + 4 * q;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gr < r_end && k < K) {
+        const float* hp = H + gr * ldh + k;
+        if (k + 3 < K) {
+          v = *reinterpret_cast<const float4*>(hp);
+        } else {
+          v.x = hp[0];
+          if (k + 1 < K) v.y = hp[1];
+          if (k + 2 < K) v.z = hp[2];
+        }
+      }
+      *reinterpret_cast<float4*>(&Hs[rr][4 * q]) = v;
+    }
+    for (int i = tid; i < RC * NP; i += 256) {       // M chunk: 32 rows x N
+      const int rr = i / NP, j = i % NP;
+      const int64_t gr = r0 + rr;
+      Ms[rr][j] = (gr < r_end && j < N) ? M[gr * ldm + j] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int rr = 0; rr < RC; ++rr) {
+      const float4 h = *reinterpret_cast<const float4*>(&Hs[rr][4 * ty]);
+      float m[TN];
+#pragma unroll
+      for (int c = 0; c < TN; ++c) m[c] = Ms[rr][tx * TN + c];
+#pragma unroll
+      for (int c = 0; c < TN; ++c) {
+        part[0][c] = fmaf(h.x, m[c], part[0][c]);
+        part[1][c] = fmaf(h.y, m[c], part[1][c]);
+        part[2][c] = fmaf(h.z, m[c], part[2][c]);
+        part[3][c] = fmaf(h.w, m[c], part[3][c]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < TN; ++c) {
+        acc[i][c] += (double)part[i][c];
+        part[i][c] = 0.f;
+      }
+  }
+  // work layout: [slice][K][NP]
+  double* wp = work + (int64_t)blockIdx.x * K * NP;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = k0 + 4 * ty + i;
+    if (k >= K) continue;
+#pragma unroll
+    for (int c = 0; c < TN; ++c) wp[(int64_t)k * NP + tx * TN + c] = acc[i][c];
+  }
+}
+
+__global__ void dense_tn_reduce_kernel(const double* __restrict__ work, int slices, int K, int NP,
+                                       int N, float* __restrict__ Y, int64_t ldy) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K * NP; i += gridDim.x * blockDim.x) {
+    const int k = i / NP, j = i % NP;
+    double s = 0.0;
+    for (int p = 0; p < slices; ++p) s += work[(int64_t)p * K * NP + i];
+    if (j < ldy) Y[(int64_t)k * ldy + j] = (j < N) ? (float)s : 0.f;
+  }
+}
+
+int tn_of(int N) { return (N + 15) / 16; }
+
+}  // namespace
+
+extern "C" {
+
+int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float* B, int64_t ldb,
+                  int32_t N, int32_t transB, float* C, int64_t ldc, float* C_relu,
+                  const float* z_mask, int64_t ld_mask, void* stream) {
+  const int TN = tn_of(N);
+  if (n < 0 || K < 1 || N < 1 || TN > 4 || (int64_t)K * 16 * TN > 16384 || (lda & 3) ||
+      ((uintptr_t)A & 15))
+    return set_err(DG_ERR_ARG, "dense_rows: shape outside the kernel's range");
+  if (n == 0) return DG_OK;
+  const size_t smem = ((size_t)K * 16 * TN + (size_t)BK * (BM + 4)) * sizeof(float);
+  const unsigned blocks = (unsigned)((n + BM - 1) / BM);
+  cudaStream_t st = S(stream);
+#define DG_DR(tn)                                                                          \
+  do {                                                                                     \
+    static bool attr = false;                                                              \
+    if (!attr) {                                                                           \
+      DG_CK(cudaFuncSetAttribute(dense_rows_kernel<tn>,                                    \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)); \
+      attr = true;                                                                         \
+    }                                                                                      \
+    dense_rows_kernel<tn><<<blocks, 256, smem, st>>>(A, lda, n, K, B, ldb, N, transB, C, ldc, \
+                                                     C_relu, z_mask, ld_mask);             \
+  } while (0)
+  switch (TN) {
+    case 1: DG_DR(1); break;
+    case 2: DG_DR(2); break;
+    case 3: DG_DR(3); break;
+    default: DG_DR(4); break;
+  }
+#undef DG_DR
+  DG_LAUNCHED();
+  return DG_OK;
+}
+
+int64_t dg_dense_tn_work(int64_t n, int32_t K, int32_t N) {
+  const int kb = (K + 63) / 64;
+  int64_t slices = std::max<int64_t>(1, (4 * 148) / kb);
+  slices = std::min<int64_t>(slices, std::max<int64_t>(1, (n + 255) / 256));
+  return slices * (int64_t)K * 16 * tn_of(N);
+}
+
+int dg_dense_tn(const float* H, int64_t ldh, int64_t n, int32_t K, const float* M, int64_t ldm,
+                int32_t N, float* Y, int64_t ldy, double* work, int64_t work_len,
+                void* stream) {
+  const int TN = tn_of(N);
+  if (n < 0 || K < 1 || N < 1 || TN > 4 || (ldh & 3) || ((uintptr_t)H & 15) || ldy > 16 * TN ||
+      ldy < N)
+    return set_err(DG_ERR_ARG, "dense_tn: shape outside the kernel's range");
+  const int kb = (K + 63) / 64;
+  int64_t slices = std::max<int64_t>(1, (4 * 148) / kb);
+  slices = std::min<int64_t>(slices, std::max<int64_t>(1, (n + 255) / 256));
+  if (work_len < slices * (int64_t)K * 16 * TN)
+    return set_err(DG_ERR_ARG, "dense_tn: work buffer too small");
+  const int64_t rows_per = std::max<int64_t>(1, (n + slices - 1) / slices);
+  const dim3 grid((unsigned)slices, (unsigned)kb);
+  cudaStream_t st = S(stream);
+  switch (TN) {
+    case 1: dense_tn_kernel<1><<<grid, 256, 0, st>>>(H, ldh, n, K, M, ldm, N, rows_per, work); break;
+    case 2: dense_tn_kernel<2><<<grid, 256, 0, st>>>(H, ldh, n, K, M, ldm, N, rows_per, work); break;
+    case 3: dense_tn_kernel<3><<<grid, 256, 0, st>>>(H, ldh, n, K, M, ldm, N, rows_per, work); break;
+    default: dense_tn_kernel<4><<<grid, 256, 0, st>>>(H, ldh, n, K, M, ldm, N, rows_per, work); break;
+  }
+  DG_LAUNCHED();
+  const int total = K * 16 * TN;
+  dense_tn_reduce_kernel<<<(unsigned)std::min(1024, (total + 255) / 256), 256, 0, st>>>(
+      work, (int)slices, K, 16 * TN, N, Y, ldy);
+  DG_LAUNCHED();
+  return DG_OK;
+}
+
+}  // extern "C"

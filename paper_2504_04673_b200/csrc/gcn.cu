@@ -105,6 +105,136 @@ __global__ void __launch_bounds__(256) xent_kernel(const float* __restrict__ x, 
   }
 }
 
+template <int G>
+__device__ __forceinline__ float grp_max(float v) {
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o, G));
+  return v;
+}
+template <int G>
+__device__ __forceinline__ double grp_sum(double v) {
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+  return v;
+}
+template <int G>
+__device__ __forceinline__ int grp_min(int v) {
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o, G));
+  return v;
+}
+
+// Vectorised variant for C <= 4*G*K: a group of G lanes owns a row, lane l
+// holds float4 chunks l, l+G, ... in registers (one pass over the row, one
+// expf per element).  Same numerics and deterministic reduction order as
+// xent_kernel (rows in order per group, groups in order per CTA, CTAs in
+// order in the last CTA).
+template <int G, int K>
+__global__ void __launch_bounds__(256) xent_vec_kernel(
+    const float* __restrict__ x, int64_t n, int C, int64_t ld, const int64_t* __restrict__ labels,
+    const uint8_t* __restrict__ mask, double denom, float* __restrict__ grad, int64_t ldg,
+    double* scratch, unsigned* counter, double* out) {
+  constexpr int RPB = 256 / G;                       // rows per CTA step
+  __shared__ double s_loss[RPB];
+  __shared__ double s_corr[RPB];
+  __shared__ bool s_last;
+  const int lig = threadIdx.x & (G - 1);
+  const int grp = threadIdx.x / G;
+  double loss = 0.0, corr = 0.0;
+  const int nchunk = (C + 3) / 4;
+  const int gchunk = (int)(ldg / 4);
+  for (int64_t row = (int64_t)blockIdx.x * RPB + grp; row < n; row += (int64_t)gridDim.x * RPB) {
+    const float4* xr = reinterpret_cast<const float4*>(x + row * ld);
+    float v[K][4];
+    float m = -INFINITY;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = lig + k * G;
+      float4 t = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      if (c < nchunk) t = xr[c];
+      v[k][0] = t.x;
+      v[k][1] = (4 * c + 1 < C) ? t.y : -INFINITY;
+      v[k][2] = (4 * c + 2 < C) ? t.z : -INFINITY;
+      v[k][3] = (4 * c + 3 < C) ? t.w : -INFINITY;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) m = fmaxf(m, v[k][e]);
+    }
+    m = grp_max<G>(m);
+    const int64_t lbl = labels[row];
+    double s = 0.0, xl = 0.0;
+    int am = C;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int j = 4 * (lig + k * G) + e;
+        if (j < C) {
+          if (v[k][e] == m && j < am) am = j;
+          if (j == lbl) xl = (double)v[k][e] - (double)m;
+          v[k][e] = expf(v[k][e] - m);
+          s += (double)v[k][e];
+        } else {
+          v[k][e] = 0.f;
+        }
+      }
+    s = grp_sum<G>(s);
+    xl = grp_sum<G>(xl);
+    am = grp_min<G>(am);
+    const bool on = mask[row] != 0;
+    const double inv_s = 1.0 / s;
+    float4* gr = reinterpret_cast<float4*>(grad + row * ldg);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int c = lig + k * G;
+      if (c < gchunk) {
+        float o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = 4 * c + e;
+          double sm = (double)v[k][e] * inv_s;
+          if (j == lbl) sm -= 1.0;
+          o[e] = (on && j < C) ? (float)(sm / denom) : 0.f;
+        }
+        gr[c] = make_float4(o[0], o[1], o[2], o[3]);
+      }
+    }
+    for (int c = lig + K * G; c < gchunk; c += G) gr[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (on) {
+      loss += log(s) - xl;
+      corr += (am == lbl) ? 1.0 : 0.0;
+    }
+  }
+  if (lig == 0) {
+    s_loss[grp] = loss;
+    s_corr[grp] = corr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double l = 0.0, c = 0.0;
+    for (int i = 0; i < RPB; ++i) {
+      l += s_loss[i];
+      c += s_corr[i];
+    }
+    scratch[2 * blockIdx.x] = l;
+    scratch[2 * blockIdx.x + 1] = c;
+    __threadfence();
+    const unsigned done = atomicAdd(counter, 1u);
+    s_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    double l = 0.0, c = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) {
+      l += ((volatile double*)scratch)[2 * b];
+      c += ((volatile double*)scratch)[2 * b + 1];
+    }
+    out[0] += l;
+    out[1] += c;
+    *counter = 0u;
+  }
+}
+
 __global__ void relu_kernel(const float4* __restrict__ z, float4* __restrict__ h, int64_t n4) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -147,9 +277,35 @@ int dg_xent(const float* logits, int64_t n, int32_t C, int64_t ld, const int64_t
             const uint8_t* mask, double denom, float* grad, int64_t ld_grad, double* scratch,
             uint32_t* counter, double* stats_out, void* stream) {
   if (n < 1 || C < 1 || C > ld || C > ld_grad) return set_err(DG_ERR_ARG, "xent: bad args");
-  const unsigned blocks = (unsigned)std::min<int64_t>((n + 7) / 8, 4 * 148);
-  xent_kernel<<<blocks, 256, 0, S(stream)>>>(logits, n, C, ld, labels, mask, denom, grad,
-                                             ld_grad, scratch, counter, stats_out);
+  const bool vec = ld % 4 == 0 && ld_grad % 4 == 0 && (((uintptr_t)logits | (uintptr_t)grad) & 15) == 0;
+  const int nchunk = (C + 3) / 4;
+  int G = 1;
+  while (G < nchunk && G < 32) G <<= 1;
+  const int K = (nchunk + G - 1) / G;
+  if (vec && K <= 4) {
+    const int rpb = 256 / G;
+    const unsigned blocks = (unsigned)std::min<int64_t>((n + rpb - 1) / rpb, 8 * 148);
+    cudaStream_t st = S(stream);
+#define DG_XV(g, k) xent_vec_kernel<g, k><<<blocks, 256, 0, st>>>(logits, n, C, ld, labels, mask, \
+                                                                  denom, grad, ld_grad, scratch, \
+                                                                  counter, stats_out)
+    switch (G) {
+      case 1: DG_XV(1, 1); break;
+      case 2: DG_XV(2, 1); break;
+      case 4: DG_XV(4, 1); break;
+      case 8: DG_XV(8, 1); break;
+      case 16: DG_XV(16, 1); break;
+      default:
+        if (K == 1) DG_XV(32, 1);
+        else if (K == 2) DG_XV(32, 2);
+        else DG_XV(32, 4);
+    }
+#undef DG_XV
+  } else {
+    const unsigned blocks = (unsigned)std::min<int64_t>((n + 7) / 8, 4 * 148);
+    xent_kernel<<<blocks, 256, 0, S(stream)>>>(logits, n, C, ld, labels, mask, denom, grad,
+                                               ld_grad, scratch, counter, stats_out);
+  }
   DG_LAUNCHED();
   return DG_OK;
 }

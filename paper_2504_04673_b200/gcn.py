@@ -208,6 +208,62 @@ def _check_train_inputs(features, labels, train_mask):
     return labels, mask
 
 
+class _Dense:
+    """The GCN step's dense transforms on the library's kernels
+    (dg_dense_rows / dg_dense_tn); cuBLAS (torch.mm, TF32 off) only for
+    shapes outside their range."""
+
+    def __init__(self, device):
+        self.device = device
+        self.work = torch.zeros(1, dtype=torch.float64, device=device)
+
+    @staticmethod
+    def _rows_ok(K, N):
+        return N <= 64 and K * 16 * ((N + 15) // 16) <= 16384
+
+    def fwd(self, t, w, f_in, f_out, relu):
+        """z = t @ w (padded), h = relu(z) if requested (gcn.py:274-276)."""
+        n, ldo = t.shape[0], w.shape[1]
+        if not self._rows_ok(f_in, f_out):
+            z = torch.mm(t, w)
+            return z, (torch.clamp_min(z, 0.0) if relu else None)
+        z = torch.empty((n, ldo), dtype=torch.float32, device=self.device)
+        h = torch.empty_like(z) if relu else None
+        L.check(L.lib().dg_dense_rows(t.data_ptr(), t.stride(0), n, f_in, w.data_ptr(),
+                                      w.stride(0), f_out, 0, z.data_ptr(), ldo,
+                                      0 if h is None else h.data_ptr(), 0, 0, L.stream_ptr()))
+        return z, h
+
+    def bwd(self, m, w, f_in, f_out, zprev):
+        """g = (m @ w^T) * 1[zprev > 0] (gcn.py:282); w is f_in x f_out."""
+        n, ldi = m.shape[0], w.shape[0]
+        if not self._rows_ok(f_out, f_in):
+            g = torch.mm(m, w.T)
+            L.check(L.lib().dg_relu_grad_mul(g.data_ptr(), g.stride(0), zprev.data_ptr(),
+                                             zprev.stride(0), n, f_in, L.stream_ptr()))
+            return g
+        g = torch.empty((n, ldi), dtype=torch.float32, device=self.device)
+        L.check(L.lib().dg_dense_rows(m.data_ptr(), m.stride(0), n, f_out, w.data_ptr(),
+                                      w.stride(0), f_in, 1, g.data_ptr(), ldi, 0,
+                                      zprev.data_ptr(), zprev.stride(0), L.stream_ptr()))
+        return g
+
+    def wgrad(self, h, m, f_in, f_out, ld_in, ld_out):
+        """y = h^T m as an (ld_in x ld_out) zero-padded matrix (gcn.py:280)."""
+        n = h.shape[0]
+        if f_out > 64 or ld_out > 16 * ((f_out + 15) // 16):
+            return torch.mm(h.T, m)
+        lib = L.lib()
+        need = int(lib.dg_dense_tn_work(n, ld_in, f_out))
+        if self.work.numel() < need:
+            self.work = torch.empty(need, dtype=torch.float64, device=self.device)
+        y = torch.empty((ld_in, ld_out), dtype=torch.float32, device=self.device)
+        L.check(lib.dg_dense_tn(h.data_ptr(), h.stride(0), n, ld_in, m.data_ptr(), m.stride(0),
+                                f_out, y.data_ptr(), ld_out, self.work.data_ptr(),
+                                self.work.numel(), L.stream_ptr()))
+        return y
+
+
 class PhaseTimer:
     """Optional CUDA-event marks between the steps of an epoch (bench
     breakdown).  `mark(name)` records an event on the current stream; the
@@ -278,6 +334,7 @@ class GcnRun:
         self.labels = torch.from_numpy(lab2.astype(np.int64)).to(dev)
         self.mask = torch.from_numpy(msk2.astype(np.uint8)).to(dev)
         self.xent = {}
+        self.dense = {}
         self.timer = None             # PhaseTimer for a breakdown run (bench)
         # register the device plans up front (multi-process: fixed IPC
         # buffers sized for the widest layer)
@@ -294,6 +351,7 @@ class GcnRun:
         yb, mb = self.labels[r0:r1], self.mask[r0:r1]
         ws = [w.clone() for w in self.w0] if weights_out is None else weights_out
         xent = self.xent.setdefault(comm.rank, _Xent(r1 - r0, self.device))
+        dense = self.dense.setdefault(comm.rank, _Dense(self.device))
         exchange_index_lists(comm, dm.fwd, cfg.variant)
         if dm.bwd is not dm.fwd:
             exchange_index_lists(comm, dm.bwd, cfg.variant)
@@ -311,15 +369,9 @@ class GcnRun:
                 for l, w in enumerate(ws):
                     t = spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant)
                     mark(f"fwd_spmm_f{dims[l]}")
-                    z = torch.mm(t, w)
+                    z, h = dense.fwd(t, w, dims[l], dims[l + 1], l < last)
                     zs.append(z)
-                    if l < last:
-                        h = torch.empty_like(z)
-                        L.check(lib.dg_relu(z.data_ptr(), h.data_ptr(), z.shape[0],
-                                            dims[l + 1], lds[l + 1], st))
-                        hs.append(h)
-                    else:
-                        hs.append(z)
+                    hs.append(h if l < last else z)
                     mark(f"fwd_dense_{l}")
                 logits = hs[-1]
                 g = torch.empty_like(logits)
@@ -328,14 +380,12 @@ class GcnRun:
                 for l in range(last, -1, -1):
                     m = spmm_phase(comm, dm.bwd, g, dims[l + 1], cfg.variant)
                     mark(f"bwd_spmm_f{dims[l + 1]}")
-                    y = comm.all_reduce_sum(torch.mm(hs[l].T, m), group=col_group,
-                                            elems=dims[l] * dims[l + 1])
+                    y = comm.all_reduce_sum(dense.wgrad(hs[l], m, dims[l], dims[l + 1], lds[l],
+                                                        lds[l + 1]),
+                                            group=col_group, elems=dims[l] * dims[l + 1])
                     mark(f"bwd_wgrad_{l}")
                     if l > 0:
-                        g = torch.mm(m, ws[l].T)
-                        L.check(lib.dg_relu_grad_mul(g.data_ptr(), g.stride(0),
-                                                     zs[l - 1].data_ptr(), zs[l - 1].stride(0),
-                                                     g.shape[0], dims[l], st))
+                        g = dense.bwd(m, ws[l], dims[l], dims[l + 1], zs[l - 1])
                     L.check(lib.dg_sgd(ws[l].data_ptr(), y.data_ptr(), ws[l].numel(),
                                        float(cfg.lr), st))
                     mark(f"bwd_dense_{l}")
