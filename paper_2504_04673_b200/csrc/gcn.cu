@@ -143,7 +143,13 @@ __global__ void __launch_bounds__(256) xent_vec_kernel(
   double loss = 0.0, corr = 0.0;
   const int nchunk = (C + 3) / 4;
   const int gchunk = (int)(ldg / 4);
-  for (int64_t row = (int64_t)blockIdx.x * RPB + grp; row < n; row += (int64_t)gridDim.x * RPB) {
+  // warp-uniform trip count: the groups of a warp share the loop (their
+  // shuffles use the full-warp mask); a group past the end runs predicated
+  const int64_t step = (int64_t)gridDim.x * RPB;
+  for (int64_t base = (int64_t)blockIdx.x * RPB + (grp & ~(32 / G - 1)); base < n; base += step) {
+    const int64_t row_raw = base + (grp & (32 / G - 1));
+    const bool valid = row_raw < n;
+    const int64_t row = valid ? row_raw : n - 1;      // in-bounds reads, no writes
     const float4* xr = reinterpret_cast<const float4*>(x + row * ld);
     float v[K][4];
     float m = -INFINITY;
@@ -180,13 +186,13 @@ __global__ void __launch_bounds__(256) xent_vec_kernel(
     s = grp_sum<G>(s);
     xl = grp_sum<G>(xl);
     am = grp_min<G>(am);
-    const bool on = mask[row] != 0;
+    const bool on = valid && mask[row] != 0;
     const double inv_s = 1.0 / s;
     float4* gr = reinterpret_cast<float4*>(grad + row * ldg);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int c = lig + k * G;
-      if (c < gchunk) {
+      if (valid && c < gchunk) {
         float o[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -198,7 +204,8 @@ __global__ void __launch_bounds__(256) xent_vec_kernel(
         gr[c] = make_float4(o[0], o[1], o[2], o[3]);
       }
     }
-    for (int c = lig + K * G; c < gchunk; c += G) gr[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid)
+      for (int c = lig + K * G; c < gchunk; c += G) gr[c] = make_float4(0.f, 0.f, 0.f, 0.f);
     if (on) {
       loss += log(s) - xl;
       corr += (am == lbl) ? 1.0 : 0.0;
