@@ -50,31 +50,46 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(
   for (int r = 0; r < 4; ++r)
 #pragma unroll
     for (int c = 0; c < TN; ++c) acc[r][c] = 0.f;
-  for (int k0 = 0; k0 < K; k0 += BK) {
-    __syncthreads();
-    // stage A[row0:row0+64, k0:k0+32] transposed: As[k][r]
-    for (int i = tid; i < BM * BK / 4; i += 256) {
+  // A chunk loader: each thread owns 2 float4 of the 64 x 32 chunk; the
+  // next chunk is loaded into registers while the current one is consumed
+  constexpr int PER = BM * BK / 4 / 256;            // float4 per thread (2)
+  auto load_chunk = [&](int k0, float4* v) {
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int i = tid + u * 256;
       const int r = i / (BK / 4), q = i % (BK / 4);
       const int64_t gr = row0 + r;
       const int k = k0 + 4 * q;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (gr < n) {
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gr < n && k < K) {
         const float* ap = A + gr * lda + k;
         if (k + 3 < K) {
-          v = *reinterpret_cast<const float4*>(ap);
+          v[u] = __ldcs(reinterpret_cast<const float4*>(ap));
         } else {
-          if (k < K) v.x = ap[0];
-          if (k + 1 < K) v.y = ap[1];
-          if (k + 2 < K) v.z = ap[2];
+          v[u].x = ap[0];
+          if (k + 1 < K) v[u].y = ap[1];
+          if (k + 2 < K) v[u].z = ap[2];
         }
       }
-      As[(4 * q + 0) * (BM + 4) + r] = v.x;
-      As[(4 * q + 1) * (BM + 4) + r] = v.y;
-      As[(4 * q + 2) * (BM + 4) + r] = v.z;
-      As[(4 * q + 3) * (BM + 4) + r] = v.w;
+    }
+  };
+  float4 nxt[PER];
+  load_chunk(0, nxt);
+  for (int k0 = 0; k0 < K; k0 += BK) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {                  // stage transposed: As[k][r]
+      const int i = tid + u * 256;
+      const int r = i / (BK / 4), q = i % (BK / 4);
+      As[(4 * q + 0) * (BM + 4) + r] = nxt[u].x;
+      As[(4 * q + 1) * (BM + 4) + r] = nxt[u].y;
+      As[(4 * q + 2) * (BM + 4) + r] = nxt[u].z;
+      As[(4 * q + 3) * (BM + 4) + r] = nxt[u].w;
     }
     __syncthreads();
+    if (k0 + BK < K) load_chunk(k0 + BK, nxt);       // in flight during the math
     const int kmax = min(BK, K - k0);
+#pragma unroll 8
     for (int kk = 0; kk < kmax; ++kk) {
       const float4 a = *reinterpret_cast<const float4*>(&As[kk * (BM + 4) + 4 * ty]);
       const float* bp = &Bs[(k0 + kk) * NP + tx * TN];
@@ -116,6 +131,7 @@ __global__ void __launch_bounds__(256) dense_tn_kernel(
   constexpr int RC = 32;                             // rows per chunk
   __shared__ __align__(16) float Hs[RC][64 + 4];
   __shared__ __align__(16) float Ms[RC][NP + 4];
+  constexpr int MPER = (RC * NP + 255) / 256;        // M elements per thread
   const int tid = threadIdx.x;
   const int tx = tid % 16;                           // n group
   const int ty = tid / 16;                           // k group (4)
@@ -131,31 +147,52 @@ __global__ void __launch_bounds__(256) dense_tn_kernel(
       part[i][c] = 0.f;
       acc[i][c] = 0.0;
     }
-  for (int64_t r0 = r_begin; r0 < r_end; r0 += RC) {
-    __syncthreads();
-    for (int i = tid; i < RC * 16; i += 256) {       // H chunk: 32 rows x 64 cols
+  // chunk loaders (H: 32 rows x 64 cols = 2 float4 per thread; M: 32 x NP);
+  // the next chunk is loaded into registers while the current is consumed
+  auto load_chunk = [&](int64_t r0, float4* hv, float* mv) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = tid + u * 256;
       const int rr = i / 16, q = i % 16;
       const int64_t gr = r0 + rr;
       const int k = k0 + 4 * q;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      hv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
       if (gr < r_end && k < K) {
         const float* hp = H + gr * ldh + k;
         if (k + 3 < K) {
-          v = *reinterpret_cast<const float4*>(hp);
+          hv[u] = __ldcs(reinterpret_cast<const float4*>(hp));
         } else {
-          v.x = hp[0];
-          if (k + 1 < K) v.y = hp[1];
-          if (k + 2 < K) v.z = hp[2];
+          hv[u].x = hp[0];
+          if (k + 1 < K) hv[u].y = hp[1];
+          if (k + 2 < K) hv[u].z = hp[2];
         }
       }
-      *reinterpret_cast<float4*>(&Hs[rr][4 * q]) = v;
     }
-    for (int i = tid; i < RC * NP; i += 256) {       // M chunk: 32 rows x N
+#pragma unroll
+    for (int u = 0; u < MPER; ++u) {
+      const int i = tid + u * 256;
       const int rr = i / NP, j = i % NP;
       const int64_t gr = r0 + rr;
-      Ms[rr][j] = (gr < r_end && j < N) ? M[gr * ldm + j] : 0.f;
+      mv[u] = (i < RC * NP && gr < r_end && j < N) ? M[gr * ldm + j] : 0.f;
+    }
+  };
+  float4 hv[2];
+  float mv[MPER];
+  if (r_begin < r_end) load_chunk(r_begin, hv, mv);
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += RC) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = tid + u * 256;
+      *reinterpret_cast<float4*>(&Hs[i / 16][4 * (i % 16)]) = hv[u];
+    }
+#pragma unroll
+    for (int u = 0; u < MPER; ++u) {
+      const int i = tid + u * 256;
+      if (i < RC * NP) Ms[i / NP][i % NP] = mv[u];
     }
     __syncthreads();
+    if (r0 + RC < r_end) load_chunk(r0 + RC, hv, mv);
 #pragma unroll 4
     for (int rr = 0; rr < RC; ++rr) {
       const float4 h = *reinterpret_cast<const float4*>(&Hs[rr][4 * ty]);

@@ -41,7 +41,7 @@ def test_full_size_checksum_and_sampled_rows(reddit, f):
     hd = torch.zeros((n, pad4(f)), device="cuda")
     hd[:, :f] = torch.from_numpy(h).cuda()
     at = P.transpose_csr(a)                       # symmetric: at == a
-    z = P.local_spmm(at, hd)                      # CUDA tensor in -> CUDA tensor out
+    z = P.local_spmm(at, hd)[:, :f]               # CUDA tensor in -> CUDA tensor out
     zc = z.double().sum(0).cpu().numpy()
     colsum_at = np.bincount(at.col_idx, weights=at.values, minlength=n)   # sum_i A^T[i, j]
     ref = colsum_at @ h.astype(np.float64)
