@@ -10,12 +10,12 @@
 // is streaming the tall operand at HBM speed, not tensor-core FLOPs.
 //
 // dg_dense_rows: a CTA owns 64 rows x all N columns; B lives in shared
-// memory (K x N <= 16K floats); A is staged in 32-wide k-chunks, transposed
+// memory (K x N <= 16K floats); A is staged in 64-wide k-chunks, transposed
 // so a thread reads 4 consecutive rows with one 16-B shared load; thread
 // tile 4 rows x N/16 columns.
 //
 // dg_dense_tn: grid = (row slices, 64-wide K blocks); each CTA accumulates
-// its slice's partial H^T M (fp32 per 32-row chunk, folded into fp64) and
+// its slice's partial H^T M (fp32 per 64-row chunk, folded into fp64) and
 // writes it to `work`; a second kernel sums the partials in slice order
 // (fp64) -- deterministic, unlike split-K with atomics.
 
@@ -24,7 +24,7 @@
 namespace {
 
 constexpr int BM = 64;   // rows per CTA (dense_rows)
-constexpr int BK = 32;   // k-chunk
+constexpr int BK = 64;   // k-chunk (4 float4 per thread in flight)
 
 template <int TN>
 __global__ void __launch_bounds__(256) dense_rows_kernel(
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(
     for (int c = 0; c < TN; ++c) acc[r][c] = 0.f;
   // A chunk loader: each thread owns 2 float4 of the 64 x 32 chunk; the
   // next chunk is loaded into registers while the current one is consumed
-  constexpr int PER = BM * BK / 4 / 256;            // float4 per thread (2)
+  constexpr int PER = BM * BK / 4 / 256;            // float4 per thread (4)
   auto load_chunk = [&](int k0, float4* v) {
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(256) dense_tn_kernel(
     const float* __restrict__ H, int64_t ldh, int64_t n, int K, const float* __restrict__ M,
     int64_t ldm, int N, int64_t rows_per, double* __restrict__ work) {
   constexpr int NP = 16 * TN;
-  constexpr int RC = 32;                             // rows per chunk
+  constexpr int RC = 64;                             // rows per chunk
   __shared__ __align__(16) float Hs[RC][64 + 4];
   __shared__ __align__(16) float Ms[RC][NP + 4];
   constexpr int MPER = (RC * NP + 255) / 256;        // M elements per thread
@@ -147,11 +147,11 @@ __global__ void __launch_bounds__(256) dense_tn_kernel(
       part[i][c] = 0.f;
       acc[i][c] = 0.0;
     }
-  // chunk loaders (H: 32 rows x 64 cols = 2 float4 per thread; M: 32 x NP);
+  // chunk loaders (H: 64 rows x 64 cols = 4 float4 per thread; M: 64 x NP);
   // the next chunk is loaded into registers while the current is consumed
   auto load_chunk = [&](int64_t r0, float4* hv, float* mv) {
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const int i = tid + u * 256;
       const int rr = i / 16, q = i % 16;
       const int64_t gr = r0 + rr;
@@ -176,13 +176,13 @@ __global__ void __launch_bounds__(256) dense_tn_kernel(
       mv[u] = (i < RC * NP && gr < r_end && j < N) ? M[gr * ldm + j] : 0.f;
     }
   };
-  float4 hv[2];
+  float4 hv[4];
   float mv[MPER];
   if (r_begin < r_end) load_chunk(r_begin, hv, mv);
   for (int64_t r0 = r_begin; r0 < r_end; r0 += RC) {
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < 4; ++u) {
       const int i = tid + u * 256;
       *reinterpret_cast<float4*>(&Hs[i / 16][4 * (i % 16)]) = hv[u];
     }

@@ -134,7 +134,9 @@ __global__ void __launch_bounds__(256) xent_vec_kernel(
     const float* __restrict__ x, int64_t n, int C, int64_t ld, const int64_t* __restrict__ labels,
     const uint8_t* __restrict__ mask, double denom, float* __restrict__ grad, int64_t ldg,
     double* scratch, unsigned* counter, double* out) {
-  constexpr int RPB = 256 / G;                       // rows per CTA step
+  constexpr int GPW = 32 / G;                        // groups per warp
+  constexpr int RPB = 256 / G;                       // groups per CTA
+  constexpr int RU = 4;                              // rows per group per step (loads batched)
   __shared__ double s_loss[RPB];
   __shared__ double s_corr[RPB];
   __shared__ bool s_last;
@@ -144,71 +146,85 @@ __global__ void __launch_bounds__(256) xent_vec_kernel(
   const int nchunk = (C + 3) / 4;
   const int gchunk = (int)(ldg / 4);
   // warp-uniform trip count: the groups of a warp share the loop (their
-  // shuffles use the full-warp mask); a group past the end runs predicated
-  const int64_t step = (int64_t)gridDim.x * RPB;
-  for (int64_t base = (int64_t)blockIdx.x * RPB + (grp & ~(32 / G - 1)); base < n; base += step) {
-    const int64_t row_raw = base + (grp & (32 / G - 1));
-    const bool valid = row_raw < n;
-    const int64_t row = valid ? row_raw : n - 1;      // in-bounds reads, no writes
-    const float4* xr = reinterpret_cast<const float4*>(x + row * ld);
-    float v[K][4];
-    float m = -INFINITY;
+  // shuffles use the full-warp mask); rows past the end run predicated.
+  // A warp covers RU consecutive blocks of GPW rows per step.
+  const int warp = threadIdx.x >> 5;
+  const int64_t step = (int64_t)gridDim.x * (256 / 32) * GPW * RU;
+  for (int64_t base = ((int64_t)blockIdx.x * (256 / 32) + warp) * GPW * RU; base < n;
+       base += step) {
+    float v[RU][K][4];
+    int64_t rowu[RU];
+    bool valid[RU];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int c = lig + k * G;
-      float4 t = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
-      if (c < nchunk) t = xr[c];
-      v[k][0] = t.x;
-      v[k][1] = (4 * c + 1 < C) ? t.y : -INFINITY;
-      v[k][2] = (4 * c + 2 < C) ? t.z : -INFINITY;
-      v[k][3] = (4 * c + 3 < C) ? t.w : -INFINITY;
+    for (int u = 0; u < RU; ++u) {                   // all loads first
+      const int64_t rr = base + u * GPW + (grp % GPW);
+      valid[u] = rr < n;
+      rowu[u] = valid[u] ? rr : n - 1;
+      const float4* xr = reinterpret_cast<const float4*>(x + rowu[u] * ld);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) m = fmaxf(m, v[k][e]);
-    }
-    m = grp_max<G>(m);
-    const int64_t lbl = labels[row];
-    double s = 0.0, xl = 0.0;
-    int am = C;
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int j = 4 * (lig + k * G) + e;
-        if (j < C) {
-          if (v[k][e] == m && j < am) am = j;
-          if (j == lbl) xl = (double)v[k][e] - (double)m;
-          v[k][e] = expf(v[k][e] - m);
-          s += (double)v[k][e];
-        } else {
-          v[k][e] = 0.f;
-        }
+      for (int k = 0; k < K; ++k) {
+        const int c = lig + k * G;
+        float4 t = make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+        if (c < nchunk) t = xr[c];
+        v[u][k][0] = t.x;
+        v[u][k][1] = (4 * c + 1 < C) ? t.y : -INFINITY;
+        v[u][k][2] = (4 * c + 2 < C) ? t.z : -INFINITY;
+        v[u][k][3] = (4 * c + 3 < C) ? t.w : -INFINITY;
       }
-    s = grp_sum<G>(s);
-    xl = grp_sum<G>(xl);
-    am = grp_min<G>(am);
-    const bool on = valid && mask[row] != 0;
-    const double inv_s = 1.0 / s;
-    float4* gr = reinterpret_cast<float4*>(grad + row * ldg);
+    }
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int c = lig + k * G;
-      if (valid && c < gchunk) {
-        float o[4];
+    for (int u = 0; u < RU; ++u) {
+      const int64_t row = rowu[u];
+      float m = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) m = fmaxf(m, v[u][k][e]);
+      m = grp_max<G>(m);
+      const int64_t lbl = labels[row];
+      double s = 0.0, xl = 0.0;
+      int am = C;
+#pragma unroll
+      for (int k = 0; k < K; ++k)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int j = 4 * c + e;
-          double sm = (double)v[k][e] * inv_s;
-          if (j == lbl) sm -= 1.0;
-          o[e] = (on && j < C) ? (float)(sm / denom) : 0.f;
+          const int j = 4 * (lig + k * G) + e;
+          if (j < C) {
+            if (v[u][k][e] == m && j < am) am = j;
+            if (j == lbl) xl = (double)v[u][k][e] - (double)m;
+            v[u][k][e] = expf(v[u][k][e] - m);
+            s += (double)v[u][k][e];
+          } else {
+            v[u][k][e] = 0.f;
+          }
         }
-        gr[c] = make_float4(o[0], o[1], o[2], o[3]);
+      s = grp_sum<G>(s);
+      xl = grp_sum<G>(xl);
+      am = grp_min<G>(am);
+      const bool on = valid[u] && mask[row] != 0;
+      const double inv_s = 1.0 / s;
+      float4* gr = reinterpret_cast<float4*>(grad + row * ldg);
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int c = lig + k * G;
+        if (valid[u] && c < gchunk) {
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int j = 4 * c + e;
+            double sm = (double)v[u][k][e] * inv_s;
+            if (j == lbl) sm -= 1.0;
+            o[e] = (on && j < C) ? (float)(sm / denom) : 0.f;
+          }
+          gr[c] = make_float4(o[0], o[1], o[2], o[3]);
+        }
       }
-    }
-    if (valid)
-      for (int c = lig + K * G; c < gchunk; c += G) gr[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (on) {
-      loss += log(s) - xl;
-      corr += (am == lbl) ? 1.0 : 0.0;
+      if (valid[u])
+        for (int c = lig + K * G; c < gchunk; c += G) gr[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (on) {
+        loss += log(s) - xl;
+        corr += (am == lbl) ? 1.0 : 0.0;
+      }
     }
   }
   if (lig == 0) {
@@ -290,7 +306,7 @@ int dg_xent(const float* logits, int64_t n, int32_t C, int64_t ld, const int64_t
   while (G < nchunk && G < 32) G <<= 1;
   const int K = (nchunk + G - 1) / G;
   if (vec && K <= 4) {
-    const int rpb = 256 / G;
+    const int rpb = (256 / G) * 4;                   // rows per CTA step (RU = 4)
     const unsigned blocks = (unsigned)std::min<int64_t>((n + rpb - 1) / rpb, 8 * 148);
     cudaStream_t st = S(stream);
 #define DG_XV(g, k) xent_vec_kernel<g, k><<<blocks, 256, 0, st>>>(logits, n, C, ld, labels, mask, \
