@@ -10,7 +10,7 @@
 // is streaming the tall operand at HBM speed, not tensor-core FLOPs.
 //
 // dg_dense_rows: a CTA owns 64 rows x all N columns; B lives in shared
-// memory (K x N <= 16K floats); A is staged in 64-wide k-chunks, transposed
+// memory (K x N <= 16K floats); A is staged in 32-wide k-chunks, transposed
 // so a thread reads 4 consecutive rows with one 16-B shared load; thread
 // tile 4 rows x N/16 columns.
 //
@@ -24,7 +24,7 @@
 namespace {
 
 constexpr int BM = 64;   // rows per CTA (dense_rows)
-constexpr int BK = 64;   // k-chunk (4 float4 per thread in flight)
+constexpr int BK = 32;   // k-chunk (2 float4 per thread in flight)
 
 template <int TN>
 __global__ void __launch_bounds__(256) dense_rows_kernel(
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(
     for (int c = 0; c < TN; ++c) acc[r][c] = 0.f;
   // A chunk loader: each thread owns 2 float4 of the 64 x 32 chunk; the
   // next chunk is loaded into registers while the current one is consumed
-  constexpr int PER = BM * BK / 4 / 256;            // float4 per thread (4)
+  constexpr int PER = BM * BK / 4 / 256;            // float4 per thread (2)
   auto load_chunk = [&](int k0, float4* v) {
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
