@@ -310,6 +310,18 @@ def run_ours(args, wl):
     launches = _lib.launch_count() - l0
     res = gr.result(holder["run"], args.steps)
 
+    # ---- extension: the same training with the transform-first order
+    #      (A^T (H W); not the reference's order -- reported separately) ----
+    import dataclasses
+    tf_ms = None
+    if not args.no_transform_first:
+        gr_tf = GcnRun.__new__(GcnRun)
+        gr_tf.__dict__.update(gr.__dict__)
+        gr_tf.cfg = dataclasses.replace(cfg, order="transform-first")
+        gr_tf.xent, gr_tf.dense = {}, {}
+        gr_tf.run(2)
+        tf_ms = _timed(lambda: gr_tf.run(args.steps), 1, w) / args.steps
+
     # ---- per-phase breakdown of one extra epoch (CUDA events between steps)
     from paper_2504_04673_b200.gcn import PhaseTimer
     gr.timer = PhaseTimer()
@@ -411,6 +423,11 @@ def run_ours(args, wl):
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
         "epoch_breakdown_ms": breakdown,
+        "extension_transform_first": None if tf_ms is None else {
+            "epoch_ms": round(tf_ms, 3),
+            "note": "TrainConfig(order='transform-first'): A^T (H W) for width-reducing layers; "
+                    "same function, forward exchange at the narrow width (volume below the "
+                    "reference's aware count); not the reference's order, not the headline"},
         "clocks": clocks,
         "loss": [round(v, 6) for v in res.losses.tolist()],
         "nnz": int(a_hat.nnz),
@@ -431,6 +448,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ranks-per-gpu", type=int, default=1)
     ap.add_argument("--c", type=int, default=1, help="1.5D replication factor")
+    ap.add_argument("--no-transform-first", action="store_true")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":

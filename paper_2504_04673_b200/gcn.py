@@ -48,6 +48,12 @@ class TrainConfig:
     variant: str = "1d-sparse"
     f_in: int = None
     f_out: int = None
+    # extension (not in the reference): "transform-first" computes
+    # A^T (H W) instead of (A^T H) W for layers that shrink the width --
+    # the same function, with the forward multiply (and its exchange) at the
+    # narrower width; the backward pass is unchanged.  Default: the
+    # reference's aggregate-first order (gcn.py:273-274), exact volumes.
+    order: str = "aggregate-first"
 
     def __post_init__(self):
         if self.layers < 2:
@@ -60,6 +66,8 @@ class TrainConfig:
             raise ValueError("epochs must be non-negative")
         if self.activation != "relu":
             raise ValueError(f"unsupported activation {self.activation!r}")
+        if self.order not in ("aggregate-first", "transform-first"):
+            raise ValueError(f"unknown order {self.order!r}")
 
     def layer_dims(self, f_in, f_out):
         return [f_in] + [self.hidden] * (self.layers - 2) + [f_out]
@@ -367,9 +375,19 @@ class GcnRun:
                 mark("epoch_start")
                 hs, zs = [h0], []
                 for l, w in enumerate(ws):
-                    t = spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant)
-                    mark(f"fwd_spmm_f{dims[l]}")
-                    z, h = dense.fwd(t, w, dims[l], dims[l + 1], l < last)
+                    if cfg.order == "transform-first" and dims[l + 1] < dims[l]:
+                        u, _ = dense.fwd(hs[-1], w, dims[l], dims[l + 1], False)
+                        z = spmm_phase(comm, dm.fwd, u, dims[l + 1], cfg.variant)
+                        mark(f"fwd_spmm_f{dims[l + 1]}_tf")
+                        h = None
+                        if l < last:
+                            h = torch.empty_like(z)
+                            L.check(lib.dg_relu(z.data_ptr(), h.data_ptr(), z.shape[0],
+                                                dims[l + 1], lds[l + 1], st))
+                    else:
+                        t = spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant)
+                        mark(f"fwd_spmm_f{dims[l]}")
+                        z, h = dense.fwd(t, w, dims[l], dims[l + 1], l < last)
                     zs.append(z)
                     hs.append(h if l < last else z)
                     mark(f"fwd_dense_{l}")

@@ -204,3 +204,22 @@ def test_softmax_xent_and_serial_gcn_api():
     np.testing.assert_allclose(out, [[1.0, 0.0]], atol=1e-7)
     with pytest.raises(RuntimeError, match="before forward"):
         P.SerialGcn(P.csr_from_dense(np.eye(2)), [np.eye(2)]).backward(np.zeros((2, 2)))
+
+
+def test_transform_first_order_same_function(gcn_golden):
+    """Extension: A^T (H W) instead of (A^T H) W -- same losses / weights as
+    the reference within fp32 tolerance; lower forward volume."""
+    g = gcn_golden
+    for key in ("g0", "g2", "g4"):
+        a = g.csr(key + "__a", P.CsrMatrix)
+        p, c, layers, hidden, epochs, seed, vi = (int(x) for x in g[key + "__cfg"])
+        variant = (P.VARIANTS + ("serial",))[vi]
+        part = None if p // c == 1 else _part(g, key, a.n_rows, p // c)
+        base = dict(layers=layers, hidden=hidden, lr=float(g[key + "__lr"][0]), epochs=epochs,
+                    seed=seed, variant=variant)
+        res = P.train(a, g[key + "__x"], g[key + "__y"], g[key + "__mask"],
+                      P.TrainConfig(order="transform-first", **base), p=p, c=c, partition=part)
+        np.testing.assert_allclose(res.losses, g[key + "__loss"], rtol=RTOL, atol=0)
+        for li, w in enumerate(res.weights):
+            ref = g[f"{key}__w{li}"]
+            np.testing.assert_allclose(w, ref, rtol=RTOL, atol=RTOL * np.abs(ref).max())
