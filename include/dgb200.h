@@ -165,6 +165,18 @@ int dg_host_permute(int64_t n, const int64_t* row_ptr, const int64_t* col, const
                     const int64_t* perm, int64_t* out_row_ptr, int64_t* out_col,
                     double* out_val);
 
+/* ---- host preprocessing: the reference's partitioners, same visiting
+ *      orders / tie-breaks / float64 comparisons (identical assignments).
+ *      greedy_tv_partition (partition.py:257-339) over the symmetric
+ *      pattern `p*` (no diagonal); volume_balanced_refine (partition.py:
+ *      342-428) over A (`a*`), A^T (`at*`) and the pattern's row_ptr.     */
+int dg_host_greedy_tv(int64_t n, const int64_t* pat_row_ptr, const int64_t* pat_col, int32_t k,
+                      double epsilon, int32_t max_passes, int64_t* assignment, int32_t* relaxed);
+int dg_host_gvb(int64_t n, const int64_t* a_row_ptr, const int64_t* a_col,
+                const int64_t* at_row_ptr, const int64_t* at_col, const int64_t* pat_row_ptr,
+                int32_t k, double lambda_max, double epsilon, int32_t max_passes,
+                int64_t* assignment);
+
 #ifdef __cplusplus
 }
 #endif

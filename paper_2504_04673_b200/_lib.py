@@ -68,6 +68,10 @@ _SIGS = {
     "dg_diag_gather": (C.c_int, [c_vp, C.c_int64, c_vp, C.c_int64, C.c_int32, C.c_int64,
                                  C.c_int32, c_vp, c_vp]),
     "dg_host_permute": (C.c_int, [C.c_int64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "dg_host_greedy_tv": (C.c_int, [C.c_int64, c_vp, c_vp, C.c_int32, C.c_double, C.c_int32,
+                                    c_vp, c_vp]),
+    "dg_host_gvb": (C.c_int, [C.c_int64, c_vp, c_vp, c_vp, c_vp, c_vp, C.c_int32, C.c_double,
+                              C.c_double, C.c_int32, c_vp]),
     "dg_host_transpose": (C.c_int, [C.c_int64, C.c_int64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
 }
 

@@ -6,8 +6,9 @@ Mirrors the partition API the hot path consumes (partition.py:19-30):
 preprocessing, vectorised (O(nnz)) instead of the reference's per-vertex
 Python loops.  The reference's partitioners (`greedy_tv_partition`,
 `volume_balanced_refine`, partition.py:257-428) are one-time host
-preprocessing outside the hot path; their output is consumed through
-`Partition.from_assignment` / `read_partition`.
+preprocessing outside the hot path; they run natively (csrc/partition.cu,
+identical assignments) so the volume-balanced configurations are feasible
+at millions of vertices.
 """
 
 from __future__ import annotations
@@ -19,7 +20,12 @@ import numpy as np
 from .sparse import CsrMatrix
 
 __all__ = ["CommMetrics", "Partition", "apply_partition", "block_partition", "comm_metrics",
-           "edgecut", "imbalance_pct", "random_partition", "read_partition", "write_partition"]
+           "edgecut", "greedy_tv_partition", "imbalance_pct", "random_partition", "read_partition",
+           "volume_balanced_refine", "write_partition"]
+
+import logging
+
+log = logging.getLogger(__name__)
 
 
 def _bounds(sizes):
@@ -227,3 +233,72 @@ def read_partition(path, k=None) -> Partition:
 
 def write_partition(path, part: Partition):
     np.savetxt(path, part.assignment, fmt="%d")
+
+
+def _sym_pattern(a: CsrMatrix) -> CsrMatrix:
+    """Undirected pattern of a (union with its transpose), diagonal removed
+    (partition.py:174-183)."""
+    from .sparse import transpose_csr
+    at = transpose_csr(a)
+    rows = a.row_of_nnz()
+    if np.array_equal(at.row_ptr, a.row_ptr) and np.array_equal(at.col_idx, a.col_idx):
+        keep = rows != a.col_idx                          # structurally symmetric
+        r, c = rows[keep], a.col_idx[keep]
+    else:
+        r = np.concatenate([rows, a.col_idx])
+        c = np.concatenate([a.col_idx, rows])
+        keep = r != c
+        key = np.unique(r[keep] * a.n_rows + c[keep])
+        r, c = key // a.n_rows, key % a.n_rows
+    rp = np.zeros(a.n_rows + 1, dtype=np.int64)
+    if r.size:
+        np.cumsum(np.bincount(r, minlength=a.n_rows), out=rp[1:])
+    return CsrMatrix(a.n_rows, a.n_cols, rp, c, np.ones(c.size), check=False)
+
+
+def greedy_tv_partition(a: CsrMatrix, k, epsilon=0.10, max_passes=10) -> Partition:
+    """BFS-grown parts refined by greedy edgecut-reducing moves
+    (partition.py:257-289), run natively with the reference's orders and
+    tie-breaks."""
+    from . import _lib as L
+    if a.n_rows != a.n_cols:
+        raise ValueError("partitioning requires a square matrix")
+    n = a.n_rows
+    _check_kn(n, k)
+    pat = _sym_pattern(a)
+    asg = np.empty(n, dtype=np.int64)
+    relaxed = np.zeros(1, dtype=np.int32)
+    rc = L.host_lib().dg_host_greedy_tv(n, pat.row_ptr.ctypes.data, pat.col_idx.ctypes.data, k,
+                                        float(epsilon), int(max_passes), asg.ctypes.data,
+                                        relaxed.ctypes.data)
+    if rc != 0:
+        raise ValueError(L.host_lib().dg_last_error().decode())
+    if relaxed[0]:
+        w = np.maximum(np.diff(pat.row_ptr), 1)
+        log.warning("a single vertex carries %d nonzeros, above the balance cap %.1f; "
+                    "relaxing the constraint to row granularity", int(w.max()),
+                    (1.0 + epsilon) * w.sum() / k)
+    return Partition.from_assignment(asg, k)
+
+
+def volume_balanced_refine(a: CsrMatrix, part: Partition, lambda_max=None, epsilon=0.10,
+                           max_passes=10) -> Partition:
+    """Boundary refinement of total and bottleneck send volume
+    (partition.py:342-428), run natively with the reference's orders and
+    tie-breaks."""
+    from . import _lib as L
+    from .sparse import transpose_csr
+    if a.n_rows != a.n_cols or a.n_rows != part.n:
+        raise ValueError("partition does not match the matrix")
+    n, k = part.n, part.k
+    lam = float(k) if lambda_max is None else float(lambda_max)
+    at = transpose_csr(a)
+    pat = _sym_pattern(a)
+    asg = part.assignment.astype(np.int64).copy()
+    arrs = [np.ascontiguousarray(x, dtype=np.int64) for x in
+            (a.row_ptr, a.col_idx, at.row_ptr, at.col_idx, pat.row_ptr)]
+    rc = L.host_lib().dg_host_gvb(n, *[x.ctypes.data for x in arrs], k, lam, float(epsilon),
+                                  int(max_passes), asg.ctypes.data)
+    if rc != 0:
+        raise ValueError(L.host_lib().dg_last_error().decode())
+    return Partition.from_assignment(asg, k)

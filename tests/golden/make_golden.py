@@ -185,3 +185,47 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def make_partition_golden():
+    """greedy_tv_partition / volume_balanced_refine assignments from the real
+    reference on a few seeded graphs (pins the native partitioners)."""
+    sys.path.insert(0, REF)
+    from distgcn import graphgen
+    from distgcn.partition import greedy_tv_partition, volume_balanced_refine
+    from distgcn.sparse import csr_from_dense, gcn_normalize
+    out = {}
+    graphs = {
+        "sbm": graphgen.sbm(120, blocks=4, seed=3)[0],
+        "star_aug": graphgen.star_augmented(150, seed=1),
+        "grid": graphgen.grid2d(9, 11),
+        "directed": None,
+    }
+    rng = np.random.default_rng(77)
+    d = (rng.random((90, 90)) < 0.05).astype(float)
+    np.fill_diagonal(d, 0.0)
+    graphs["directed"] = csr_from_dense(d)
+    keys = []
+    for name, a in graphs.items():
+        for k, extra in ((3, {}), (4, {"lambda_max": 2.0}), (6, {"epsilon": 0.3})):
+            for norm in (False, True):
+                a2 = gcn_normalize(a) if norm else a
+                tag = f"{name}_k{k}_{int(norm)}"
+                g = greedy_tv_partition(a2, k, epsilon=extra.get("epsilon", 0.10))
+                v = volume_balanced_refine(a2, g, lambda_max=extra.get("lambda_max"),
+                                           epsilon=extra.get("epsilon", 0.10))
+                out[tag + "__rp"] = a2.row_ptr
+                out[tag + "__ci"] = a2.col_idx
+                out[tag + "__v"] = a2.values
+                out[tag + "__n"] = np.array([a2.n_rows, a2.n_cols])
+                out[tag + "__cfg"] = np.array([k, extra.get("lambda_max", -1.0),
+                                               extra.get("epsilon", 0.10)])
+                out[tag + "__greedy"] = g.assignment
+                out[tag + "__gvb"] = v.assignment
+                keys.append(tag)
+    out["cases"] = np.array(keys)
+    np.savez_compressed(os.path.join(HERE, "partition_golden.npz"), **out)
+
+
+if __name__ == "__main__":
+    make_partition_golden()
