@@ -82,6 +82,33 @@ def _make_spmm_plan(rank_ops, max_chunk, flags=0):
     return h
 
 
+def _check_bounds(vplan, local):
+    """Host-side bounds validation of everything the kernels will index
+    (compute-sanitizer is unavailable on the GPU pool): extended columns
+    inside [0, n_local + halo_rows), row pointers monotone and covering the
+    entries, every exchange segment inside its source block and its
+    destination halo."""
+    for r in local:
+        ro = vplan.ranks[r]
+        if ro.col_ext.size:
+            lo, hi = int(ro.col_ext.min()), int(ro.col_ext.max())
+            if lo < 0 or hi >= ro.n_local + ro.halo_rows:
+                raise ValueError(f"rank {r}: extended column {lo}..{hi} outside "
+                                 f"[0, {ro.n_local + ro.halo_rows})")
+        if ro.row_ptr[0] != 0 or ro.row_ptr[-1] != ro.col_ext.size or \
+                np.any(np.diff(ro.row_ptr) < 0):
+            raise ValueError(f"rank {r}: malformed row pointers")
+    widths = vplan.widths
+    for sg in vplan.segments:
+        if sg.dst_row0 < 0 or sg.dst_row0 + sg.count > vplan.ranks[sg.dst].halo_rows:
+            raise ValueError(f"segment {sg.src}->{sg.dst} overflows the receiver's halo")
+        if sg.idx is not None and sg.idx.size and (int(sg.idx.min()) < 0 or
+                                                   int(sg.idx.max()) >= widths[sg.q]):
+            raise ValueError(f"segment {sg.src}->{sg.dst} indexes outside block {sg.q}")
+        if sg.idx is None and sg.count > widths[sg.q]:
+            raise ValueError(f"segment {sg.src}->{sg.dst} longer than block {sg.q}")
+
+
 class _Part:
     """A rank operand restricted to its own-block (interior) or halo
     (boundary) entries, storage order kept."""
@@ -122,6 +149,7 @@ class DevicePlan:
         self.acc = acc
         self.device = torch.device("cuda", torch.cuda.current_device())
         ro = [vplan.ranks[r] for r in self.local]
+        _check_bounds(vplan, self.local)
         self.overlap = self.multi
         if self.overlap:
             self._splan = _make_spmm_plan([_Part(x, False) for x in ro], max_chunk)
