@@ -98,7 +98,7 @@ def _check_bounds(vplan, local):
         if ro.row_ptr[0] != 0 or ro.row_ptr[-1] != ro.col_ext.size or \
                 np.any(np.diff(ro.row_ptr) < 0):
             raise ValueError(f"rank {r}: malformed row pointers")
-    widths = vplan.widths
+    widths = getattr(vplan, "widths", None)
     for sg in vplan.segments:
         if sg.dst_row0 < 0 or sg.dst_row0 + sg.count > vplan.ranks[sg.dst].halo_rows:
             raise ValueError(f"segment {sg.src}->{sg.dst} overflows the receiver's halo")
