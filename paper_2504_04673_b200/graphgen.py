@@ -280,3 +280,45 @@ def community_partition(communities, k):
         bounds.append((pos, pos + int(sz)))
         pos += int(sz)
     return Partition(comm.size, k, asg, perm, bounds)
+
+
+# ---------------------------------------------------------------------------
+# the reference's small generators (graphgen.py:52-120), same draw sequences
+# ---------------------------------------------------------------------------
+
+def grid2d(rows, cols) -> CsrMatrix:
+    """4-neighbour lattice, row-major numbering (graphgen.py:52-65)."""
+    idx = np.arange(rows * cols, dtype=np.int64).reshape(rows, cols)
+    u = np.concatenate([idx[:, :-1].ravel(), idx[:-1, :].ravel()])
+    v = np.concatenate([idx[:, 1:].ravel(), idx[1:, :].ravel()])
+    return symmetric_unit(rows * cols, u, v)
+
+
+def star(leaves) -> CsrMatrix:
+    """Vertex 0 joined to `leaves` leaves (graphgen.py:68-72)."""
+    return symmetric_unit(leaves + 1, np.zeros(leaves, np.int64),
+                          np.arange(1, leaves + 1, dtype=np.int64))
+
+
+def star_augmented(n, seed=0, community_fracs=(0.35, 0.25, 0.2, 0.12, 0.08), avg_degree=8.0,
+                   p_out=0.002, hubs=3, hub_frac=0.15) -> CsrMatrix:
+    """Unequal communities plus global hubs (graphgen.py:88-120)."""
+    rng = np.random.default_rng(seed)
+    sizes = [max(2, int(round(f * n))) for f in community_fracs]
+    sizes[-1] = n - sum(sizes[:-1])
+    if sizes[-1] < 2:
+        raise ValueError("n too small for the community layout")
+    labels = np.repeat(np.arange(len(sizes)), sizes)
+    p_in = np.minimum(avg_degree / np.maximum(np.array(sizes) - 1, 1), 1.0)
+    prob = np.where(labels[:, None] == labels[None, :], p_in[labels][:, None], p_out)
+    draw = rng.random((n, n))
+    rows, cols = np.nonzero(np.triu(draw < prob, k=1))
+    starts = np.concatenate([[0], np.cumsum(sizes)[:-1]])
+    hr, hc = [rows], [cols]
+    for h in range(min(hubs, len(sizes))):
+        hub = int(starts[h])
+        targets = rng.choice(n, size=max(1, int(hub_frac * n)), replace=False)
+        targets = targets[targets != hub]
+        hr.append(np.full(targets.size, hub, dtype=np.int64))
+        hc.append(targets.astype(np.int64))
+    return symmetric_unit(n, np.concatenate(hr), np.concatenate(hc))
