@@ -286,10 +286,16 @@ def run_ours(args, wl):
                         variant=args.variant)
     part = None
     part_name = "block"
-    if args.workload in _COMM and p // c > 1:
+    k = p // c
+    if args.partition == "gvb" and k > 1:
+        # the reference's greedy-tv -> GVB (partition.py:257-428), run natively
+        t_p = time.time()
+        part = P.volume_balanced_refine(a_hat, P.greedy_tv_partition(a_hat, k))
+        part_name = f"greedy-tv -> GVB (native, {time.time() - t_p:.0f}s host)"
+    elif args.workload in _COMM and k > 1:
         from paper_2504_04673_b200.graphgen import community_partition
-        part = community_partition(_COMM[args.workload], p // c)
-        part_name = "planted-community (stand-in for METIS/GVB)"
+        part = community_partition(_COMM[args.workload], k)
+        part_name = "planted-community (stand-in for METIS)"
     gr = GcnRun(a_hat, x, y, mask, cfg, p=p, c=c, partition=part)
     log(f"[bench] proc {w.proc}: setup {time.time() - t_setup:.1f}s")
     dims = gr.dims
@@ -449,6 +455,9 @@ def main():
     ap.add_argument("--ranks-per-gpu", type=int, default=1)
     ap.add_argument("--c", type=int, default=1, help="1.5D replication factor")
     ap.add_argument("--no-transform-first", action="store_true")
+    ap.add_argument("--partition", default="auto", choices=["auto", "gvb"],
+                    help="auto: block (Reddit) / planted communities (products); "
+                         "gvb: the reference's greedy-tv -> GVB")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
