@@ -137,13 +137,15 @@ class DevicePlan:
     exchange + device barrier run on a side stream, and a halo (boundary)
     pass that accumulates into Z once the barrier has passed."""
 
-    def __init__(self, vplan, local_ranks=None, acc=ACC_FP64, max_chunk=MAX_CHUNK, max_ld=None):
+    def __init__(self, vplan, local_ranks=None, acc=ACC_FP64, max_chunk=MAX_CHUNK, max_ld=None,
+                 standalone=False):
         from .dist import world
         lib = L.lib()
         self.vplan = vplan
         self.grid = vplan.grid
         self.world = world()
-        self.multi = self.world.multi
+        # standalone: a process-local plan (local_spmm) -- never collective
+        self.multi = self.world.multi and not standalone
         self.local = list(range(vplan.grid.p)) if local_ranks is None else list(local_ranks)
         self.li = {r: k for k, r in enumerate(self.local)}
         self.acc = acc
@@ -418,10 +420,22 @@ def reduce_members(tensors):
     return res
 
 
+class _LocalPlan:
+    """A one-rank VariantPlan whose columns are all local (local_spmm)."""
+
+    def __init__(self, ro):
+        from .runtime import ProcessGrid
+        self.grid = ProcessGrid(1, 1)
+        self.ranks = [ro]
+        self.segments = []
+        self.widths = [ro.n_local]
+        self.variant = "1d-sparse"
+
+
 def single_spmm(a, h):
-    """`local_spmm` on one GPU: one rank whose columns are all local."""
+    """`local_spmm` on one GPU: one rank whose columns are all local; a
+    process-local plan (no collective, also under torchrun)."""
     from .plan import RankOperand
-    from .runtime import ProcessGrid
     if getattr(h, "ndim", None) != 2 and not (isinstance(h, torch.Tensor) and h.dim() == 2):
         raise ValueError("dense operand must be 2-D")
     if a.n_cols != h.shape[0]:
@@ -434,15 +448,7 @@ def single_spmm(a, h):
         return z if numpy_in else torch.zeros((a.n_rows, f), device=h.device)
     ro = RankOperand(0, 0, 0, a.n_rows, a.n_cols, a.row_ptr,
                      a.col_idx.astype(np.int32), a.values.astype(np.float32), 0, {})
-
-    class _VP:
-        pass
-    vp = _VP()
-    vp.grid = ProcessGrid(1, 1)
-    vp.ranks = [ro]
-    vp.segments = []
-    vp.variant = "1d-sparse"
-    plan = DevicePlan(vp)
+    plan = DevicePlan(_LocalPlan(ro), standalone=True)
     hd = to_device(h, ld)
     z = plan.run({0: hd}, f, ld)[0][:, :f]
     return z.double().cpu().numpy() if numpy_in else z
