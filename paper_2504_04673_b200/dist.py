@@ -132,6 +132,22 @@ class SymBuffer:
                     L.check(lib.dg_ipc_open_handle((C.c_uint8 * 64)(*hb), C.byref(out)))
                     self.ptrs.append(out.value)
 
+    def close(self, world: "World"):
+        """Collective release: unmap the peers' buffers, wait until every
+        process has done the same, then free the local buffer (a peer must
+        never touch freed memory)."""
+        if self.local is None:
+            return
+        lib = L.lib()
+        if world.multi:
+            torch.cuda.synchronize()
+            for q, ptr in enumerate(self.ptrs):
+                if q != world.proc:
+                    L.check(lib.dg_ipc_close(C.c_void_p(ptr)))
+            world.host_barrier()
+        L.check(lib.dg_free(C.c_void_p(self.local)))
+        self.local, self.ptrs = None, []
+
     def tensor(self, numel, dtype=torch.float32, offset_bytes=0):
         """The local buffer as a torch tensor view (no copy)."""
         return _as_tensor(self.local + offset_bytes, numel, dtype)

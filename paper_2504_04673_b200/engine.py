@@ -222,14 +222,27 @@ class DevicePlan:
         return (self.psym.ptrs[q] + self._poff[r]
                 + par * self.vplan.ranks[r].n_rows * self.max_ld * 4)
 
+    def close(self):
+        """Release device state.  Multi-process: collective (every process
+        closes the same plans in the same order)."""
+        if self.multi:
+            for buf in (getattr(self, "hsym", None), getattr(self, "psym", None)):
+                if buf is not None:
+                    buf.close(self.world)
+            self.hsym = self.psym = None
+        self._destroy_plans()
+
+    def _destroy_plans(self):
+        lib = L.lib()
+        for name in ("_splan", "_bplan", "_xplan"):
+            h = getattr(self, name, None)
+            if h:
+                (lib.dg_xchg_plan_destroy if name == "_xplan" else lib.dg_spmm_plan_destroy)(h)
+                setattr(self, name, None)
+
     def __del__(self):
         try:
-            lib = L.lib()
-            for h in (getattr(self, "_splan", None), getattr(self, "_bplan", None)):
-                if h:
-                    lib.dg_spmm_plan_destroy(h)
-            if getattr(self, "_xplan", None):
-                lib.dg_xchg_plan_destroy(self._xplan)
+            self._destroy_plans()
         except Exception:  # noqa: BLE001 - interpreter teardown
             pass
 
@@ -375,6 +388,12 @@ class GroupReducer:
             counts[q] += 1
         self.sym = SymBuffer(self.w, max(2 * counts[self.w.proc] * self.slot, 16))
         self.parity = 0
+
+    def close(self):
+        """Collective release of the symmetric slots."""
+        if self.sym is not None:
+            self.sym.close(self.w)
+            self.sym = None
 
     def _ptr(self, r, par):
         q = self.w.proc_of(r, self.p)

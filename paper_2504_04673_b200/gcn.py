@@ -452,7 +452,9 @@ def train(a_hat: CsrMatrix, features, labels, train_mask, cfg: TrainConfig, p=1,
         return serial_train(a_hat, features, labels, train_mask, cfg)
     gr = GcnRun(a_hat, features, labels, train_mask, cfg, p, c, partition)
     run = gr.run()
-    return gr.result(run)
+    res = gr.result(run)
+    gr.dm.release_device()
+    return res
 
 
 def serial_train(a_hat: CsrMatrix, features, labels, train_mask, cfg: TrainConfig) -> TrainResult:
@@ -461,6 +463,7 @@ def serial_train(a_hat: CsrMatrix, features, labels, train_mask, cfg: TrainConfi
     c2 = replace(cfg, variant="1d-sparse")
     gr = GcnRun(a_hat, features, labels, train_mask, c2, 1, 1, None)
     res = gr.result(gr.run())
+    gr.dm.release_device()
     for row in res.history:
         for k in [k for k in row if k.endswith("_bytes")]:
             del row[k]

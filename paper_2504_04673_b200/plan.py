@@ -85,6 +85,12 @@ class DistOperand:
     def n_blocks(self) -> int:
         return len(self.boundaries)
 
+    def release_device(self):
+        """Free the cached device plans (collective under torchrun)."""
+        for dp in self._device.values():
+            dp.close()
+        self._device.clear()
+
     @property
     def blocks(self):
         if self._blocks is None:
@@ -120,6 +126,11 @@ class DistMatrices:
     @property
     def symmetric(self) -> bool:
         return self.bwd is self.fwd
+
+    def release_device(self):
+        self.fwd.release_device()
+        if self.bwd is not self.fwd:
+            self.bwd.release_device()
 
 
 def build_dist_matrices(a: CsrMatrix, boundaries, grid: ProcessGrid) -> DistMatrices:

@@ -150,6 +150,7 @@ def run_spmm(a: CsrMatrix, h, p, c, variant, partition=None, index_setup=True) -
     dev = hd.device
     z2 = torch.cat([run.results[grid.rank_of(i, 0)].to(dev) for i in range(grid.n_rows)],
                    0)[:, :f]
+    dm.release_device()
     if not part.is_identity:
         z2 = z2[torch.from_numpy(part.perm).to(z2.device)]
     z = z2.double().cpu().numpy() if numpy_in else z2
