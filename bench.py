@@ -382,19 +382,44 @@ def run_ours(args, wl):
                 "f": f0}
 
     # ---- end to end through the public API with host buffers ------------
+    # Every step uploads its inputs (the hosted block rows of the features)
+    # from pinned host memory and reads the loss back.  The upload for step
+    # k+1 runs on a copy stream into the second of two device buffers while
+    # epoch k computes (double-buffered input pipeline); step 0's upload is
+    # exposed.  All copies are inside the timed region.
     rows = [gr.dm.boundaries[grid.coords(r)[0]] for r in dp.local]
     xh = {r: gr.x[r0:r1].cpu().pin_memory() for r, (r0, r1) in zip(dp.local, rows)}
-    e2e_steps = max(1, min(args.steps, 5))
+    xbuf = [gr.x, torch.empty_like(gr.x)]
+    copy_stream = torch.cuda.Stream()
+    e2e_steps = max(2, min(args.steps, 6))
     d2h = [0]
+    state = {"k": 0, "ev": None}
+
+    def upload(buf, stream):
+        with torch.cuda.stream(stream):
+            for r, (r0, r1) in zip(dp.local, rows):
+                buf[r0:r1].copy_(xh[r], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        return ev
 
     def e2e_step():
-        for r, (r0, r1) in zip(dp.local, rows):
-            gr.x[r0:r1].copy_(xh[r], non_blocking=True)
+        k = state["k"]
+        cur = xbuf[k % 2]
+        if k == 0:
+            state["ev"] = upload(cur, torch.cuda.current_stream())
+        torch.cuda.current_stream().wait_event(state["ev"])
+        if k + 1 < e2e_steps:                     # prefetch the next step's inputs
+            copy_stream.wait_stream(torch.cuda.current_stream())
+            state["ev"] = upload(xbuf[(k + 1) % 2], copy_stream)
+        gr.x = cur
         rr = gr.run(1)
         st = rr.results[grid.rank_of(0, 0)]["stats"].cpu()   # loss / correct to host
         d2h[0] += st.numel() * st.element_size()
+        state["k"] = k + 1
 
     e2e_ms = _timed(e2e_step, e2e_steps, w)
+    gr.x = xbuf[0]
     h2d = sum(w.all_gather_object(sum(v.numel() * 4 for v in xh.values())))
 
     # ---- CPU baseline (rank 0, N=1 only) --------------------------------
