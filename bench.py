@@ -292,10 +292,11 @@ def run_ours(args, wl):
         t_p = time.time()
         part = P.volume_balanced_refine(a_hat, P.greedy_tv_partition(a_hat, k))
         part_name = f"greedy-tv -> GVB (native, {time.time() - t_p:.0f}s host)"
-    elif args.workload in _COMM and k > 1:
+    elif args.workload in _COMM:
+        # community-ordered layout (also for a single part: locality)
         from paper_2504_04673_b200.graphgen import community_partition
         part = community_partition(_COMM[args.workload], k)
-        part_name = "planted-community (stand-in for METIS)"
+        part_name = "planted-community, community-ordered (stand-in for METIS)"
     gr = GcnRun(a_hat, x, y, mask, cfg, p=p, c=c, partition=part)
     log(f"[bench] proc {w.proc}: setup {time.time() - t_setup:.1f}s")
     dims = gr.dims
