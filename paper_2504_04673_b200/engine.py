@@ -265,14 +265,19 @@ class DevicePlan:
                                         len(self.local), L.ptr_array(dst), len(dst), f, ld,
                                         1 if self.multi else 0, stream))
 
-    def run(self, hs: dict, f: int, ld: int, out: dict = None) -> dict:
+    def run(self, hs: dict, f: int, ld: int, out: dict = None, reduce: bool = True) -> dict:
         """One multiply phase.  hs[r]: (n_i, ld) fp32 CUDA tensor for every
-        hosted rank r; returns {r: (n_i, ld) tensor}."""
+        hosted rank r; returns {r: (n_i, ld) tensor}.  1.5D with
+        reduce=False returns each replica's partial product (views of the
+        plan's partial buffers, valid until the next phase) for a reduction
+        after the transform."""
         lib = L.lib()
         st = _stream()
         vp = self.vplan
         p = self.grid.p
-        if out is None:
+        if self.reduce and not reduce:
+            out = {}
+        elif out is None:
             out = {r: torch.empty((vp.ranks[r].n_rows, ld), dtype=torch.float32,
                                   device=self.device) for r in self.local}
         if not self.multi:
@@ -289,6 +294,9 @@ class DevicePlan:
                 zp = [out[r].data_ptr() for r in self.local]
             self._spmm(self._splan, hs, [halos[r].data_ptr() for r in self.local], zp, f, ld,
                        0, st)
+            if self.reduce and not reduce:
+                return {r: self._buffer(self.partial, r, vp.ranks[r].n_rows, ld)
+                        for r in self.local}
             if self.reduce:
                 zl = dict(zip(self.local, zp))
                 for i in range(self.grid.n_rows):
@@ -317,6 +325,11 @@ class DevicePlan:
         self._spmm(self._bplan, hs, halo_ptrs, zp, f, ld, 1, st)       # halo rows, z +=
         for r in self.local:                            # inputs in use on the side stream
             hs[r].record_stream(self._side)
+        if self.reduce and not reduce:
+            from .dist import _as_tensor
+            return {r: _as_tensor(self._partial_ptr(r, par), vp.ranks[r].n_rows * ld,
+                                  torch.float32).view(vp.ranks[r].n_rows, ld)
+                    for r in self.local}
         if self.reduce:
             self.world.barrier()                        # every replica's partial is ready
             for r in self.local:
@@ -415,6 +428,63 @@ class GroupReducer:
             L.check(lib.dg_group_reduce(len(grp), L.ptr_array([self._ptr(m, par) for m in grp]),
                                         1, L.ptr_array([o]), 0, self.numel, 0, _stream()))
             out[r] = o
+        return out
+
+
+class RowGroupReducer:
+    """Row-group sum of per-replica (n_i x ld) tensors, bit-identical on
+    every replica (ascending member order).  Multi-process: symmetric slots
+    sized for the largest block row, two parities, one device barrier."""
+
+    def __init__(self, grid, vplan, ld):
+        from .dist import SymBuffer, world
+        self.grid, self.w, self.ld = grid, world(), int(ld)
+        self.rows = {r: vplan.ranks[r].n_rows for r in range(grid.p)}
+        self.sym = None
+        if self.w.multi:
+            p = grid.p
+            self.slot = max(self.rows.values()) * self.ld * 4
+            self.idx, counts = {}, [0] * self.w.size
+            for r in range(p):
+                q = self.w.proc_of(r, p)
+                self.idx[r] = counts[q]
+                counts[q] += 1
+            self.per_par = {q: counts[q] * self.slot for q in range(self.w.size)}
+            self.sym = SymBuffer(self.w, max(2 * counts[self.w.proc] * self.slot, 16))
+        self.parity = 0
+
+    def close(self):
+        if self.sym is not None:
+            self.sym.close(self.w)
+            self.sym = None
+
+    def _ptr(self, r, par):
+        q = self.w.proc_of(r, self.grid.p)
+        return self.sym.ptrs[q] + par * self.per_par[q] + self.idx[r] * self.slot
+
+    def __call__(self, parts: dict) -> dict:
+        lib = L.lib()
+        out = {r: torch.empty_like(t) for r, t in parts.items()}
+        if not self.w.multi:
+            for i in range(self.grid.n_rows):
+                grp = self.grid.row_group(i)
+                if not all(r in parts for r in grp):
+                    continue
+                n = parts[grp[0]].numel()
+                L.check(lib.dg_group_reduce(len(grp), L.ptr_array([parts[r] for r in grp]),
+                                            len(grp), L.ptr_array([out[r] for r in grp]), 0, n,
+                                            0, _stream()))
+            return out
+        from .dist import _as_tensor
+        par = self.parity
+        self.parity ^= 1
+        for r, t in parts.items():
+            _as_tensor(self._ptr(r, par), t.numel(), torch.float32).copy_(t.reshape(-1))
+        self.w.barrier()
+        for r, t in parts.items():
+            grp = self.grid.row_group(self.grid.coords(r)[0])
+            L.check(lib.dg_group_reduce(len(grp), L.ptr_array([self._ptr(m, par) for m in grp]),
+                                        1, L.ptr_array([out[r]]), 0, t.numel(), 0, _stream()))
         return out
 
 

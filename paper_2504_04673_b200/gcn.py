@@ -28,7 +28,7 @@ from .partition import Partition, apply_partition, block_partition
 from .plan import build_dist_matrices, validate_variant_grid
 from .runtime import ProcessGrid, run_program
 from .sparse import CsrMatrix, csr_equal, local_spmm, transpose_csr
-from .spmm import exchange_index_lists, spmm_phase
+from .spmm import exchange_index_lists, row_group_reduce, spmm_phase
 
 __all__ = ["SerialGcn", "TrainConfig", "TrainResult", "init_weights", "relu", "relu_grad",
            "serial_train", "softmax_xent", "train"]
@@ -54,6 +54,11 @@ class TrainConfig:
     # narrower width; the backward pass is unchanged.  Default: the
     # reference's aggregate-first order (gcn.py:273-274), exact volumes.
     order: str = "aggregate-first"
+    # extension: in the 1.5D variants, reduce the c replica
+    # partials after the transform (n_i x f_out) instead of before it
+    # (n_i x f_in), since (sum_j T_j) W = sum_j (T_j W).  Off by default:
+    # the reference reduces before (spmm.py:227).
+    reduce_after_transform: bool = False
 
     def __post_init__(self):
         if self.layers < 2:
@@ -369,6 +374,8 @@ class GcnRun:
         lib = L.lib()
         st = L.stream_ptr()
         dims, lds = self.dims, self.lds
+        post_reduce = (cfg.reduce_after_transform and cfg.variant.startswith("15d")
+                       and comm.grid.c > 1)
         tm = self.timer if comm.rank == min(comm._rt.local) else None
         mark = tm.mark if tm is not None else (lambda name: None)
         with _no_tf32():
@@ -380,6 +387,17 @@ class GcnRun:
                         u, _ = dense.fwd(hs[-1], w, dims[l], dims[l + 1], False)
                         z = spmm_phase(comm, dm.fwd, u, dims[l + 1], cfg.variant)
                         mark(f"fwd_spmm_f{dims[l + 1]}_tf")
+                        h = None
+                        if l < last:
+                            h = torch.empty_like(z)
+                            L.check(lib.dg_relu(z.data_ptr(), h.data_ptr(), z.shape[0],
+                                                dims[l + 1], lds[l + 1], st))
+                    elif post_reduce and dims[l + 1] < dims[l]:
+                        parts = spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant,
+                                           reduce=False, reduce_f=dims[l + 1])
+                        u, _ = dense.fwd(parts, w, dims[l], dims[l + 1], False)
+                        z = row_group_reduce(comm, u, dm, cfg.variant)
+                        mark(f"fwd_spmm_f{dims[l]}_postreduce")
                         h = None
                         if l < last:
                             h = torch.empty_like(z)

@@ -181,9 +181,11 @@ class VariantPlan:
     widths: list
     nnz_cols: dict = field(repr=False, default=None)
 
-    def charge(self, ledger: CommLedger, f: int):
+    def charge(self, ledger: CommLedger, f: int, reduce_f: int = None):
         """Ledger charges of one multiply phase of width f -- exactly what
-        the reference's collectives charge for the same phase."""
+        the reference's collectives charge for the same phase.  `reduce_f`
+        (extension): the width of the 1.5D row-group reduction when it runs
+        after the transform (n_i x f_out instead of n_i x f_in)."""
         p, c = self.grid.p, self.grid.c
         allr = tuple(range(p))
         if self.variant == "1d-oblivious":
@@ -194,8 +196,9 @@ class VariantPlan:
         else:                                                     # spmm.py:203-227
             for s in self.segments:
                 ledger.p2p(s.src, s.dst, s.count * f)
+            rf = f if reduce_f is None else reduce_f
             for i in range(self.grid.n_rows):
-                ledger.allreduce(self.grid.row_group(i), self.widths[i] * f)
+                ledger.allreduce(self.grid.row_group(i), self.widths[i] * rf)
 
     def elements(self, f: int) -> int:
         """Exchanged data elements of one phase (excluding the 1.5D reduction)."""

@@ -29,7 +29,7 @@ from .sparse import CsrMatrix, local_spmm, transpose_csr
 
 __all__ = ["DistMatrices", "DistOperand", "VARIANTS", "build_dist_matrices",
            "exchange_index_lists", "run_spmm", "serial_reference", "spmm_kernel",
-           "validate_variant_grid", "SpmmRun", "device_plan", "spmm_phase"]
+           "validate_variant_grid", "SpmmRun", "device_plan", "spmm_phase", "row_group_reduce"]
 
 
 def exchange_index_lists(comm: Comm, op: DistOperand, variant: str):
@@ -65,11 +65,15 @@ def device_plan(op: DistOperand, grid: ProcessGrid, variant: str, max_ld=None):
     return dp
 
 
-def spmm_phase(comm: Comm, op: DistOperand, h_pad: torch.Tensor, f: int, variant: str):
+def spmm_phase(comm: Comm, op: DistOperand, h_pad: torch.Tensor, f: int, variant: str,
+               reduce: bool = True, reduce_f: int = None):
     """Device form of `spmm_kernel`: h_pad is a contiguous fp32 CUDA tensor
     (n_i, pad4(f)) with zero padding; returns the padded (n_i, pad4(f))
     product.  A collective over the ranks of this process: the last rank to
-    arrive launches exchange -> SpMM -> (1.5D) group reduction for all."""
+    arrive launches exchange -> SpMM -> (1.5D) group reduction for all.
+    reduce=False (1.5D, extension): return each replica's partial product;
+    the caller reduces after its transform and `reduce_f` is the width the
+    ledger charges for that reduction."""
     grid = comm.grid
     ledger = comm.ledger
     ld = pad4(f)
@@ -81,11 +85,31 @@ def spmm_phase(comm: Comm, op: DistOperand, h_pad: torch.Tensor, f: int, variant
             hs[r] = h if (isinstance(h, torch.Tensor) and h.dtype == torch.float32
                           and h.is_cuda and h.is_contiguous() and h.shape[1] == ld) \
                 else to_device(h[:, :f], ld)
-        out = dp.run(hs, f, ld)
-        dp.vplan.charge(ledger, f)
+        out = dp.run(hs, f, ld, reduce=reduce)
+        dp.vplan.charge(ledger, f, None if reduce else reduce_f)
         return out
 
-    return comm._collective(("spmm", id(op), variant), tuple(range(comm.p)), h_pad, complete)
+    return comm._collective(("spmm", id(op), variant, reduce), tuple(range(comm.p)), h_pad,
+                            complete)
+
+
+def row_group_reduce(comm: Comm, u: torch.Tensor, dm: DistMatrices, variant: str):
+    """Row-group sum of a replica-partial (n_i x ld) tensor (the reduction
+    that `spmm_phase(reduce=False)` deferred), bit-identical on the
+    replicas.  Collective over the ranks of this process."""
+    from .engine import RowGroupReducer
+    rt = comm._rt
+    ld = int(u.shape[1])
+
+    def complete(arr):
+        key = ("rowgroup", ld, id(dm))
+        red = rt.ctx.get(key)
+        if red is None:
+            red = rt.ctx[key] = RowGroupReducer(comm.grid, device_plan(
+                dm.fwd, comm.grid, variant).vplan, ld)
+        return red(dict(arr))
+
+    return comm._collective(("rowgroup", ld), tuple(range(comm.p)), u, complete)
 
 
 def spmm_kernel(comm: Comm, op: DistOperand, h_block, variant: str):

@@ -223,3 +223,29 @@ def test_transform_first_order_same_function(gcn_golden):
         for li, w in enumerate(res.weights):
             ref = g[f"{key}__w{li}"]
             np.testing.assert_allclose(w, ref, rtol=RTOL, atol=RTOL * np.abs(ref).max())
+
+
+def test_reduce_after_transform_same_function(gcn_golden):
+    """Extension: 1.5D replica reduction after the transform --
+    same losses / weights as the reference, smaller all-reduce volume."""
+    g = gcn_golden
+    for key in ("g2", "g3"):                       # 15d-sparse p=4 c=2; 15d-oblivious p=8 c=2
+        a = g.csr(key + "__a", P.CsrMatrix)
+        p, c, layers, hidden, epochs, seed, vi = (int(x) for x in g[key + "__cfg"])
+        variant = P.VARIANTS[vi]
+        part = _part(g, key, a.n_rows, p // c)
+        base = dict(layers=layers, hidden=hidden, lr=float(g[key + "__lr"][0]), epochs=epochs,
+                    seed=seed, variant=variant)
+        ref = P.train(a, g[key + "__x"], g[key + "__y"], g[key + "__mask"],
+                      P.TrainConfig(**base), p=p, c=c, partition=part)
+        res = P.train(a, g[key + "__x"], g[key + "__y"], g[key + "__mask"],
+                      P.TrainConfig(reduce_after_transform=True, **base), p=p, c=c,
+                      partition=part)
+        np.testing.assert_allclose(res.losses, g[key + "__loss"], rtol=RTOL, atol=0)
+        for li, w in enumerate(res.weights):
+            r = g[f"{key}__w{li}"]
+            np.testing.assert_allclose(w, r, rtol=RTOL, atol=RTOL * np.abs(r).max())
+        for per_rank in res.weights_per_rank[1:]:
+            for w0, wr in zip(res.weights_per_rank[0], per_rank):
+                assert np.array_equal(w0, wr)
+        assert (res.ledger.total_bytes_sent("data") <= ref.ledger.total_bytes_sent("data"))
