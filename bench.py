@@ -283,7 +283,8 @@ def run_ours(args, wl):
     p = args.gpus * args.ranks_per_gpu
     c = args.c
     cfg = P.TrainConfig(layers=wl["layers"], hidden=wl["hidden"], lr=0.01, epochs=1, seed=1,
-                        variant=args.variant)
+                        variant=args.variant,
+                        reduce_after_transform=args.reduce_after_transform)
     part = None
     part_name = "block"
     k = p // c
@@ -437,6 +438,7 @@ def run_ours(args, wl):
         "ms_per_step": round(ms_epoch, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32 (SpMM accumulates f64)", "data": "synthetic",
         "config": {"workload": wl["desc"], "variant": args.variant, "p": p, "c": c,
+                   "reduce_after_transform": bool(args.reduce_after_transform),
                    "partition": part_name,
                    "l2": "inputs larger than L2 (H0 = %d MB)" % (gr.x.numel() * 4 // 2**20),
                    "ranks_per_gpu": args.ranks_per_gpu},
@@ -481,6 +483,8 @@ def main():
     ap.add_argument("--ranks-per-gpu", type=int, default=1)
     ap.add_argument("--c", type=int, default=1, help="1.5D replication factor")
     ap.add_argument("--no-transform-first", action="store_true")
+    ap.add_argument("--reduce-after-transform", action="store_true",
+                    help="extension: 1.5D replica reduction after the transform")
     ap.add_argument("--partition", default="auto", choices=["auto", "gvb"],
                     help="auto: block (Reddit) / planted communities (products); "
                          "gvb: the reference's greedy-tv -> GVB")

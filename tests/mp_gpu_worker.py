@@ -75,6 +75,18 @@ def main():
                 if not np.array_equal(w0, wr):
                     fails.append((key, "replication"))
         n_checked += 1
+        if variant.startswith("15d") and c > 1:   # extension: post-transform reduction
+            import dataclasses
+            res2 = P.train(a, gg[key + "__x"], gg[key + "__y"], gg[key + "__mask"],
+                           dataclasses.replace(cfg, reduce_after_transform=True), p=p, c=c,
+                           partition=part)
+            if not np.allclose(res2.losses, gg[key + "__loss"], rtol=1e-5, atol=0):
+                fails.append((key, "reduce_after_transform loss", res2.losses.tolist()))
+            for per_rank in res2.weights_per_rank[1:]:
+                for w0, wr in zip(res2.weights_per_rank[0], per_rank):
+                    if not np.array_equal(w0, wr):
+                        fails.append((key, "reduce_after_transform replication"))
+            n_checked += 1
     print(f"[proc {w.proc}/{w.size}] checked {n_checked} cases, {len(fails)} failures",
           flush=True)
     for f in fails:
