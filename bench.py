@@ -68,6 +68,16 @@ def ncu_traffic(key):
         return None
 
 
+def nvlink_peak():
+    """Measured peer-copy GB/s per direction (profiles/nvlink.json, written
+    from scripts/nvlink_probe.py), else the B200_PROFILING.md figure."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "nvlink.json")) as fh:
+            return float(json.load(fh)["peer_copy_gbs"]), "measured (profiles/nvlink.json)"
+    except Exception:  # noqa: BLE001
+        return 770.0, "B200_PROFILING.md measured peer copy"
+
+
 def peaks():
     try:
         with open(PEAKS) as fh:
@@ -377,9 +387,10 @@ def run_ours(args, wl):
                 snd[qs] += sg.count
                 rcv[qd] += sg.count
         inter = max(max(snd), max(rcv)) * 4 * f0
+        nvl, nvl_src = nvlink_peak()
         exch = {"bound": "nvlink", "achieved": round(inter / t_xchg / 1e9, 1),
-                "peak": 770.0, "unit": "GB/s", "frac": round(inter / t_xchg / 1e9 / 770.0, 4),
-                "peak_source": "B200_PROFILING.md measured peer copy per direction",
+                "peak": nvl, "unit": "GB/s", "frac": round(inter / t_xchg / 1e9 / nvl, 4),
+                "peak_source": nvl_src,
                 "exchange_ms": round(t_xchg * 1e3, 3), "busiest_rank_bytes": int(inter),
                 "f": f0}
 
