@@ -146,7 +146,9 @@ int dg_xchg_run(dg_xchg_plan* p, const float* const* h_src, int n_src, float* co
   for (int i = 0; i < n_dst; ++i) a.dst[i] = dst_bufs[i];
   a.segs = p->segs;
   a.ld = ld;
-  a.chunks = (f + 3) / 4;
+  // whole 32-B chunks when the rows allow it: the SpMM's 256-bit path reads
+  // rows in 8-float units, so the halo must carry the zero padding too
+  a.chunks = (ld % 8 == 0) ? std::min<int>((int)(ld / 4), 2 * ((f + 7) / 8)) : (f + 3) / 4;
   a.fence_sys = fence_sys;
   int G = 1;
   while (G < a.chunks && G < 32) G <<= 1;
@@ -357,12 +359,56 @@ __global__ void __launch_bounds__(256) gather_probe_kernel(const float* __restri
   if (acc.x == 123.456f) out[0] = acc.y + acc.z + acc.w;   // keep the loads alive
 }
 
+// 256-bit variant: each lane loads 32 B (two float4) with one
+// ld.global.nc.v8 (Blackwell); G lanes cover 32*G bytes of a row.
+template <int G>
+__global__ void __launch_bounds__(256) gather_probe_v8_kernel(const float* __restrict__ tab,
+                                                              int64_t ld,
+                                                              const int32_t* __restrict__ idx,
+                                                              int64_t n_idx, int per_group,
+                                                              float* __restrict__ out) {
+  const int lig = threadIdx.x & (G - 1);
+  const int64_t grp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int64_t base = grp * per_group;
+  float acc = 0.f;
+  for (int k = 0; k < per_group; k += 4) {
+    int r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = __ldg(idx + ((base + k + u) % n_idx));
+    float x[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const float* p = tab + (int64_t)r[u] * ld + 8 * lig;
+      asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=f"(x[u][0]), "=f"(x[u][1]), "=f"(x[u][2]), "=f"(x[u][3]), "=f"(x[u][4]),
+                     "=f"(x[u][5]), "=f"(x[u][6]), "=f"(x[u][7])
+                   : "l"(p));
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc += x[u][e];
+  }
+  if (acc == 123.456f) out[0] = acc;
+}
+
 }  // namespace
 
 extern "C" int dg_diag_gather(const float* tab, int64_t ld, const int32_t* idx, int64_t n_idx,
                               int32_t lanes, int64_t groups, int32_t per_group, float* out,
                               void* stream) {
   const unsigned blocks = (unsigned)((groups * lanes + 255) / 256);
+  if (lanes < 0) {                       // 256-bit loads: -lanes lanes x 32 B
+    switch (-lanes) {
+      case 2: gather_probe_v8_kernel<2><<<(unsigned)((groups * 2 + 255) / 256), 256, 0, S(stream)>>>(tab, ld, idx, n_idx, per_group, out); break;
+      case 4: gather_probe_v8_kernel<4><<<(unsigned)((groups * 4 + 255) / 256), 256, 0, S(stream)>>>(tab, ld, idx, n_idx, per_group, out); break;
+      case 8: gather_probe_v8_kernel<8><<<(unsigned)((groups * 8 + 255) / 256), 256, 0, S(stream)>>>(tab, ld, idx, n_idx, per_group, out); break;
+      case 16: gather_probe_v8_kernel<16><<<(unsigned)((groups * 16 + 255) / 256), 256, 0, S(stream)>>>(tab, ld, idx, n_idx, per_group, out); break;
+      default: return set_err(DG_ERR_ARG, "diag_gather: v8 lanes must be 2, 4, 8 or 16");
+    }
+    DG_LAUNCHED();
+    return DG_OK;
+  }
   switch (lanes) {
     case 4: gather_probe_kernel<4><<<blocks, 256, 0, S(stream)>>>(tab, ld, idx, n_idx, per_group, out); break;
     case 8: gather_probe_kernel<8><<<blocks, 256, 0, S(stream)>>>(tab, ld, idx, n_idx, per_group, out); break;

@@ -86,16 +86,54 @@ __device__ __forceinline__ float4 ld_h(const float4* p) { return __ldg(p); }
 // Occupancy vs in-flight loads (measured on B200, Reddit-shaped graph):
 // one float4 chunk per lane -> 4 entries per step and >= 4 CTAs/SM (<= 64
 // registers); wider lanes keep more registers and fewer CTAs (no spills).
-template <int CPL>
+template <int CPL, int V>
 struct Tune {
   static constexpr int E = 4;                       // entries per pipeline step
-  static constexpr int MINB = CPL == 1 ? 4 : (CPL == 2 ? 2 : 1);
+  static constexpr int W = CPL * V / 4;             // float4s per lane
+  static constexpr int MINB = W == 1 ? 4 : (W == 2 ? 2 : 1);
 };
 
-template <int G, int CPL, bool F64>
-__global__ void __launch_bounds__(256, Tune<CPL>::MINB)
+// V floats per lane-chunk: 4 -> 128-bit loads (LDG.128); 8 -> Blackwell's
+// 256-bit loads (LDG.E.ENL2.256).  Measured with the gather probe (profiles/
+// r01/gather_roofline.txt): random 256-B row gathers reach 18.4 TB/s with
+// 256-bit loads vs 10.6 TB/s with 128-bit -- the 128-bit ceiling is the
+// load-instruction rate, not L2 bandwidth.  V=8 needs 32-B aligned rows.
+template <int V>
+struct Vec;
+template <>
+struct Vec<4> {
+  float v[4];
+  __device__ __forceinline__ void load(const float* p) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = t.x;
+    v[1] = t.y;
+    v[2] = t.z;
+    v[3] = t.w;
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = 0.f;
+  }
+};
+template <>
+struct Vec<8> {
+  float v[8];
+  __device__ __forceinline__ void load(const float* p) {
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+          "=f"(v[7])
+        : "l"(p));
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = 0.f;
+  }
+};
+
+template <int G, int CPL, bool F64, int V>
+__global__ void __launch_bounds__(256, (Tune<CPL, V>::MINB))
     spmm_kernel(const __grid_constant__ SpmmArgs a) {
-  constexpr int E = Tune<CPL>::E;           // entries per pipeline step
+  constexpr int E = Tune<CPL, V>::E;        // entries per pipeline step
   constexpr int E4 = E / 2;                 // int4 loads per step
   const int lig = threadIdx.x & (G - 1);
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -110,24 +148,24 @@ __global__ void __launch_bounds__(256, Tune<CPL>::MINB)
   const int64_t nl = R.n_local;
   const uint64_t pol = evict_first_policy();
 
-  int chk[CPL];
+  int chk[CPL];                             // chunk index (units of V floats)
   bool on[CPL];
 #pragma unroll
   for (int q = 0; q < CPL; ++q) {
     chk[q] = slab0 + lig + q * G;
     on[q] = chk[q] < a.chunks && (lig + q * G) < a.slab;
   }
-  float part[CPL][4];
-  double acc[F64 ? CPL : 1][4];
+  float part[CPL][V];
+  double acc[F64 ? CPL : 1][V];
 #pragma unroll
   for (int q = 0; q < CPL; ++q)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) part[q][k] = 0.f;
+    for (int k = 0; k < V; ++k) part[q][k] = 0.f;
   if constexpr (F64) {
 #pragma unroll
     for (int q = 0; q < CPL; ++q)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc[q][k] = 0.0;
+      for (int k = 0; k < V; ++k) acc[q][k] = 0.0;
   }
 
   const int len = it.len;
@@ -149,7 +187,7 @@ __global__ void __launch_bounds__(256, Tune<CPL>::MINB)
       }
     }
     const int nv = min(E, len - s * E);
-    float4 x[E][CPL];
+    Vec<V> x[E][CPL];
     float v[E];
 #pragma unroll
     for (int j = 0; j < E; ++j) {
@@ -158,29 +196,27 @@ __global__ void __launch_bounds__(256, Tune<CPL>::MINB)
       if (j < nv) {
         const float* hp = c < nl ? hl + (int64_t)c * ld : hh + (int64_t)(c - nl) * ld;
 #pragma unroll
-        for (int q = 0; q < CPL; ++q)
-          x[j][q] = on[q] ? ld_h(reinterpret_cast<const float4*>(hp) + chk[q])
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < CPL; ++q) {
+          if (on[q]) x[j][q].load(hp + (int64_t)chk[q] * V);
+          else x[j][q].zero();
+        }
       } else {
         v[j] = 0.f;
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) x[j][q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = 0; q < CPL; ++q) x[j][q].zero();
       }
     }
 #pragma unroll
     for (int j = 0; j < E; ++j)
 #pragma unroll
-      for (int q = 0; q < CPL; ++q) {
-        part[q][0] = fmaf(v[j], x[j][q].x, part[q][0]);
-        part[q][1] = fmaf(v[j], x[j][q].y, part[q][1]);
-        part[q][2] = fmaf(v[j], x[j][q].z, part[q][2]);
-        part[q][3] = fmaf(v[j], x[j][q].w, part[q][3]);
-      }
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int k = 0; k < V; ++k) part[q][k] = fmaf(v[j], x[j][q].v[k], part[q][k]);
     if constexpr (F64) {
 #pragma unroll
       for (int q = 0; q < CPL; ++q)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < V; ++k) {
           acc[q][k] += (double)part[q][k];
           part[q][k] = 0.f;
         }
@@ -192,41 +228,55 @@ __global__ void __launch_bounds__(256, Tune<CPL>::MINB)
 #pragma unroll
     for (int q = 0; q < CPL; ++q)
       if (on[q]) {
-        float4 o;
-        float4* zq = reinterpret_cast<float4*>(zp) + chk[q];
-        if constexpr (F64) {
-          if (a.beta) {
-            const float4 zo = *zq;
-            acc[q][0] += (double)zo.x;
-            acc[q][1] += (double)zo.y;
-            acc[q][2] += (double)zo.z;
-            acc[q][3] += (double)zo.w;
-          }
-          o = make_float4((float)acc[q][0], (float)acc[q][1], (float)acc[q][2], (float)acc[q][3]);
-        } else {
-          o = make_float4(part[q][0], part[q][1], part[q][2], part[q][3]);
-          if (a.beta) {
-            const float4 zo = *zq;
-            o.x += zo.x;
-            o.y += zo.y;
-            o.z += zo.z;
-            o.w += zo.w;
+        float o[V];
+        float4* zq = reinterpret_cast<float4*>(zp + (int64_t)chk[q] * V);
+#pragma unroll
+        for (int k = 0; k < V; ++k) {
+          if constexpr (F64) {
+            o[k] = (float)acc[q][k];
+          } else {
+            o[k] = part[q][k];
           }
         }
-        *zq = o;
+        if (a.beta) {                       // z += result (halo pass)
+#pragma unroll
+          for (int h4 = 0; h4 < V / 4; ++h4) {
+            const float4 zo = zq[h4];
+            if constexpr (F64) {
+              o[4 * h4 + 0] = (float)(acc[q][4 * h4 + 0] + (double)zo.x);
+              o[4 * h4 + 1] = (float)(acc[q][4 * h4 + 1] + (double)zo.y);
+              o[4 * h4 + 2] = (float)(acc[q][4 * h4 + 2] + (double)zo.z);
+              o[4 * h4 + 3] = (float)(acc[q][4 * h4 + 3] + (double)zo.w);
+            } else {
+              o[4 * h4 + 0] += zo.x;
+              o[4 * h4 + 1] += zo.y;
+              o[4 * h4 + 2] += zo.z;
+              o[4 * h4 + 3] += zo.w;
+            }
+          }
+        }
+#pragma unroll
+        for (int h4 = 0; h4 < V / 4; ++h4)
+          zq[h4] = make_float4(o[4 * h4], o[4 * h4 + 1], o[4 * h4 + 2], o[4 * h4 + 3]);
       }
   } else {
     double* pp = a.part + (int64_t)it.slot * a.ld_part;
 #pragma unroll
     for (int q = 0; q < CPL; ++q)
       if (on[q]) {
-        double4 d;
-        if constexpr (F64) {
-          d = make_double4(acc[q][0], acc[q][1], acc[q][2], acc[q][3]);
-        } else {
-          d = make_double4(part[q][0], part[q][1], part[q][2], part[q][3]);
+        double4* dq = reinterpret_cast<double4*>(pp + (int64_t)chk[q] * V);
+#pragma unroll
+        for (int h4 = 0; h4 < V / 4; ++h4) {
+          double4 d;
+          if constexpr (F64) {
+            d = make_double4(acc[q][4 * h4], acc[q][4 * h4 + 1], acc[q][4 * h4 + 2],
+                             acc[q][4 * h4 + 3]);
+          } else {
+            d = make_double4(part[q][4 * h4], part[q][4 * h4 + 1], part[q][4 * h4 + 2],
+                             part[q][4 * h4 + 3]);
+          }
+          dq[h4] = d;
         }
-        reinterpret_cast<double4*>(pp)[chk[q]] = d;
       }
   }
 }
@@ -258,19 +308,19 @@ int bucket_of(int32_t len) {
   return (int)(4.0 * std::log2((double)len)) + 1;
 }
 
-template <int G, int CPL, bool F64>
+template <int G, int CPL, bool F64, int V>
 void launch_spmm(const SpmmArgs& a, int nslabs, cudaStream_t s) {
   const int64_t threads = a.n_items * G;
   const unsigned gx = (unsigned)((threads + 255) / 256);
-  spmm_kernel<G, CPL, F64><<<dim3(gx, nslabs), 256, 0, s>>>(a);
+  spmm_kernel<G, CPL, F64, V><<<dim3(gx, nslabs), 256, 0, s>>>(a);
 }
 
 using LaunchFn = void (*)(const SpmmArgs&, int, cudaStream_t);
 
-template <bool F64>
+template <bool F64, int V>
 LaunchFn pick_launch(int G, int CPL) {
 #define DG_CASE(g, c) \
-  if (G == g && CPL == c) return &launch_spmm<g, c, F64>;
+  if (G == g && CPL == c) return &launch_spmm<g, c, F64, V>;
   DG_CASE(1, 1) DG_CASE(1, 2) DG_CASE(1, 3) DG_CASE(1, 4)
   DG_CASE(2, 1) DG_CASE(2, 2) DG_CASE(2, 3) DG_CASE(2, 4)
   DG_CASE(4, 1) DG_CASE(4, 2) DG_CASE(4, 3) DG_CASE(4, 4)
@@ -457,7 +507,15 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   if (!p) return set_err(DG_ERR_ARG, "dg_spmm_run: null plan");
   if (f < 1 || ld_h % 4 || ld_z % 4 || f > ld_h || f > ld_z)
     return set_err(DG_ERR_ARG, "dg_spmm_run: need 1 <= f <= ld, ld % 4 == 0");
-  const int chunks = (f + 3) / 4;
+  // 256-bit lane chunks when rows are >= 32 floats and 32-B aligned
+  bool v8 = f > 16 && ld_h % 8 == 0 && ld_z % 8 == 0;
+  for (int r = 0; r < p->n_ranks && v8; ++r) {
+    const uintptr_t al = (uintptr_t)h_local[r] | (uintptr_t)z[r] |
+                         (uintptr_t)(h_halo ? h_halo[r] : nullptr);
+    v8 = (al & 31) == 0;
+  }
+  const int V = v8 ? 8 : 4;
+  const int chunks = (f + V - 1) / V;
   SpmmArgs a;
   std::memset(&a, 0, sizeof(a));
   int64_t ext_total = 0;
@@ -481,7 +539,7 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   }
   int wmax;
   if (slab_floats > 0) {
-    wmax = std::max(1, slab_floats / 4);
+    wmax = std::max(1, slab_floats / V);
   } else {
     // Slabs pay off only when a slab of >= 128 B per gathered row stays
     // L2-resident (~64 MB of the 126 MB L2; measured on B200: Reddit-shaped
@@ -489,9 +547,10 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
     // fit, the gathers hit DRAM whatever the slab, and one wide slab
     // (fewest CSR passes, widest G) wins.
     const double budget = 64.0 * 1024 * 1024;
-    const double per_chunk = (double)std::max<int64_t>(ext_total, 1) * 16.0;
+    const double per_chunk = (double)std::max<int64_t>(ext_total, 1) * 4.0 * V;
     const int fit = (int)std::max(0.0, budget / per_chunk);
-    wmax = fit >= 8 ? fit : 128;
+    const int min_w = 32 / V;                     // >= 128 B of every row per slab
+    wmax = fit >= min_w ? fit : 128;
   }
   int G, CPL, ns;
   choose_config(chunks, wmax, &G, &CPL, &ns);
@@ -505,7 +564,8 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   a.slab = G * CPL;
   a.beta = beta ? 1 : 0;
   if (p->n_items == 0) return DG_OK;
-  LaunchFn fn = acc ? pick_launch<true>(G, CPL) : pick_launch<false>(G, CPL);
+  LaunchFn fn = v8 ? (acc ? pick_launch<true, 8>(G, CPL) : pick_launch<false, 8>(G, CPL))
+                   : (acc ? pick_launch<true, 4>(G, CPL) : pick_launch<false, 4>(G, CPL));
   if (!fn) return set_err(DG_ERR_ARG, "dg_spmm_run: no kernel for config");
   fn(a, ns, S(stream));
   DG_LAUNCHED();
@@ -517,7 +577,7 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
     fa.part = p->part;
     fa.ld_z = ld_z;
     fa.ld_part = ld_h;
-    fa.nfloat = chunks * 4;
+    fa.nfloat = std::min<int>(chunks * V, (int)ld_z);
     fa.beta = beta ? 1 : 0;
     spmm_fixup_kernel<<<(unsigned)p->n_fix, 128, 0, S(stream)>>>(fa);
     DG_LAUNCHED();

@@ -37,11 +37,16 @@ MAX_CHUNK = 1024      # nonzeros per work item before a row is split
 
 
 def pad4(f: int) -> int:
-    """Row pitch (floats) of an f-wide dense operand: 16-byte rows, and
-    128-byte (cache-line) rows for wide layers (f > 64) so a feature slab
-    of a multiple of 32 floats maps onto whole L2 lines."""
+    """Row pitch (floats) of an f-wide dense operand: 16-byte rows for
+    f <= 16; 32-byte rows for f <= 64 (the SpMM's 256-bit loads); 128-byte
+    (cache-line) rows for wide layers, so a feature slab of a multiple of 32
+    floats maps onto whole L2 lines."""
     f = int(f)
-    return (f + 31) // 32 * 32 if f > 64 else (f + 3) // 4 * 4
+    if f > 64:
+        return (f + 31) // 32 * 32
+    if f > 16:
+        return (f + 7) // 8 * 8
+    return (f + 3) // 4 * 4
 
 
 def to_device(h, ld=None, device=None) -> torch.Tensor:

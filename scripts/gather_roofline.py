@@ -19,11 +19,15 @@ def main():
     out = torch.zeros(4, device="cuda")
     for rows, ld, lanes in [(232965, 16, 4), (232965, 44, 8), (232965, 608, 16),
                             (232965, 608, 32), (232965, 64, 16), (2449029, 16, 4),
-                            (2449029, 100, 16), (1 << 22, 64, 16)]:
+                            (2449029, 100, 16), (1 << 22, 64, 16),
+                            # 256-bit loads (negative lanes: -lanes lanes x 32 B)
+                            (232965, 16, -2), (232965, 64, -8), (232965, 32, -4),
+                            (232965, 608, -8)]:
         tab = torch.randn(rows, ld, device="cuda")
         idx = torch.randint(0, rows, (n_idx,), device="cuda", dtype=torch.int32)
         per_group = 64
-        groups = 148 * 64 * 8 * 8 // lanes * 4
+        lanes_n = abs(lanes)
+        groups = 148 * 64 * 8 * 8 // lanes_n * 4
         def go():
             L.check(lib.dg_diag_gather(tab.data_ptr(), ld, idx.data_ptr(), n_idx, lanes, groups,
                                        per_group, out.data_ptr(), L.stream_ptr()))
@@ -37,9 +41,10 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         t = e0.elapsed_time(e1) / reps / 1e3
-        nbytes = groups * per_group * lanes * 16
+        nbytes = groups * per_group * (lanes_n * 32 if lanes < 0 else lanes * 16)
         foot = rows * ld * 4 / 2**20
-        print(f"rows={rows} ld={ld} row_bytes={lanes*16} footprint={foot:.0f}MiB: "
+        rb = lanes_n * 32 if lanes < 0 else lanes * 16
+        print(f"rows={rows} ld={ld} row_bytes={rb} v8={lanes < 0} footprint={foot:.0f}MiB: "
               f"{nbytes / t / 1e9:.0f} GB/s gathered", flush=True)
         del tab, idx
 
