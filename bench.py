@@ -47,6 +47,11 @@ WORKLOADS = {
                           "hidden communities), f_in=100, 3-layer GCN (layers=4, hidden=16), C=47, "
                           "community-preserving partition",
                      n=2_449_029, f_in=100, classes=47, layers=4, hidden=16),
+    "papers": dict(desc="ogbn-papers100M-shaped power-law graph (111,059,956 vertices, ~3.23B "
+                        "stored off-diagonal nonzeros + self-loops, Chung-Lu alpha=0.7, degree cap "
+                        "30,000), f_in=128, 3-layer GCN (layers=4, hidden=16), C=172, block "
+                        "partition, built sharded in HBM (sharded.py)",
+                   n=111_059_956, f_in=128, classes=172, layers=4, hidden=16),
 }
 
 
@@ -163,7 +168,7 @@ class ClockSampler:
 # reference arm / cpu baseline: the oracle port on a bounded sample
 # ---------------------------------------------------------------------------
 
-def cpu_reference_epoch_ms(a_hat, wl, budget_s=20.0):
+def cpu_reference_epoch_ms(a_hat, wl, budget_s=20.0, nnz_total=None):
     """Time the reference's CPU hot loop (np.add.at local_spmm, sparse.py:222,
     via the oracle port) on row samples of the same graph at each SpMM
     width of the epoch, then extrapolate the full epoch:
@@ -173,7 +178,7 @@ def cpu_reference_epoch_ms(a_hat, wl, budget_s=20.0):
     import distgcn_oracle as O
     dims = [wl["f_in"]] + [wl["hidden"]] * (wl["layers"] - 2) + [wl["classes"]]
     widths = dims[:-1] + dims[1:]           # forward widths, then backward widths
-    nnz_total = a_hat.nnz
+    nnz_total = a_hat.nnz if nnz_total is None else int(nnz_total)
     rates = {}
     per_width = budget_s / len(set(widths))
     rng = np.random.default_rng(0)
@@ -245,6 +250,9 @@ def spmm_bytes(vp, rank, f):
     """Compulsory bytes of one rank's local SpMM:
     4(m+1) + 8 nnz + 4 f u + 4 f m, with u = distinct gathered rows."""
     ro = vp.ranks[rank]
+    if getattr(ro, "col_ext", None) is None:       # HBM-resident operand: counts kept
+        m, nnz, u = ro.n_rows, ro.nnz, ro.u
+        return 4 * (m + 1) + 8 * nnz + 4 * f * u + 4 * f * m, u, nnz, m
     m, nnz = ro.n_rows, ro.col_ext.size
     key = (id(vp), rank)
     if key not in _U:
@@ -272,8 +280,156 @@ def _timed(fn, reps, w):
     return max(w.all_gather_object(ms))
 
 
+def _papers_sample(g, rows_target_nnz=6_000_000):
+    """Leading rows of the first hosted block (columns compacted) as a host
+    CsrMatrix: the CPU reference's rate sample for the papers-shaped graph."""
+    import paper_2504_04673_b200 as P
+    i = min(g.blocks)
+    rp, col, val = g.blocks[i]
+    k = int(np.searchsorted(rp, rows_target_nnz))
+    k = max(1, min(k, len(rp) - 1))
+    nz = int(rp[k])
+    c = col[:nz].long().cpu().numpy()
+    uniq, cc = np.unique(c, return_inverse=True)
+    return P.CsrMatrix(k, uniq.size, rp[:k + 1].copy(), cc.astype(np.int64),
+                       val[:nz].double().cpu().numpy(), check=False)
+
+
+def run_papers(args, wl):
+    """Config 5 (ogbn-papers100M-shaped): the graph, features and labels are
+    generated sharded -- every process builds only its hosted block rows, in
+    HBM (sharded.py) -- then the same GcnRun epoch loop is timed."""
+    import torch
+    import paper_2504_04673_b200 as P
+    from paper_2504_04673_b200 import _lib, sharded
+    from paper_2504_04673_b200.dist import world
+    from paper_2504_04673_b200.engine import pad4
+    from paper_2504_04673_b200.gcn import PhaseTimer
+    from paper_2504_04673_b200.spmm import device_plan
+
+    w = world().init()
+    if w.size != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={w.size}")
+    if args.variant not in ("1d-sparse", "1d-oblivious") or args.c != 1:
+        raise SystemExit("papers workload: 1D variants only")
+    lead = w.proc == 0
+    p = args.gpus * args.ranks_per_gpu
+    t0 = time.time()
+    g = sharded.papers_shaped_sharded(p, seed=0, log=log if lead else None)
+    t_gen = time.time() - t0
+    log(f"[bench] proc {w.proc}: papers graph nnz={g.nnz_total:,} ({t_gen:.0f}s), "
+        f"mem {torch.cuda.memory_allocated() / 2**30:.1f} GiB")
+    sample = _papers_sample(g) if lead else None
+    x, y = sharded.sharded_inputs(g, wl["f_in"], wl["classes"], seed=1)
+    cfg = P.TrainConfig(layers=wl["layers"], hidden=wl["hidden"], lr=0.01, epochs=1, seed=1,
+                        variant=args.variant)
+    gr = sharded.sharded_gcn_run(g, x, y, wl["f_in"], wl["classes"], cfg)
+    t_setup = time.time() - t0
+    log(f"[bench] proc {w.proc}: setup {t_setup:.0f}s, "
+        f"mem {torch.cuda.memory_allocated() / 2**30:.1f} GiB")
+    dims, grid = gr.dims, gr.grid
+    gr.run(args.warmup)
+    torch.cuda.synchronize()
+    w.host_barrier()
+    l0 = _lib.launch_count()
+    clk = ClockSampler(torch.cuda.current_device())
+    holder = {}
+    ms_epoch = _timed(lambda: holder.__setitem__("run", gr.run(args.steps)), 1, w) / args.steps
+    clocks = clk.stop()
+    launches = _lib.launch_count() - l0
+    res = gr.result(holder["run"], args.steps)
+    peak_mem = max(w.all_gather_object(torch.cuda.max_memory_allocated()))
+    gr.timer = PhaseTimer()
+    gr.run(1)
+    breakdown = {k: round(v, 3) for k, v in gr.timer.summary().items()}
+    gr.timer = None
+    # ---- dominant kernel: the 128-wide forward SpMM of layer 1 ---------
+    dp = device_plan(gr.dm.fwd, grid, args.variant)
+    f0, ld0 = dims[0], pad4(dims[0])
+    hs = {r: gr.x[r] for r in dp.local}
+    zs = {r: torch.empty_like(hs[r]) for r in dp.local}
+    dp.exchange_only(hs, f0, ld0)
+    dp.spmm_only(hs, f0, ld0, zs)
+    t_spmm = _timed(lambda: dp.spmm_only(hs, f0, ld0, zs), 3, w) / 1e3
+    t_xchg = _timed(lambda: dp.exchange_only(hs, f0, ld0), 3, w) / 1e3 if p > 1 else None
+    del zs
+    tot_b = gather_b = 0
+    for r in dp.local:
+        b, u, nnz, m = spmm_bytes(dp.vplan, r, f0)
+        tot_b += b
+        gather_b += 4 * (m + 1) + 8 * nnz + 4 * f0 * nnz + 4 * f0 * m
+    peak, peak_src = peaks()
+    achieved = tot_b / t_spmm / 1e9
+    widths = dims[:-1] + dims[1:]
+    spmm_bytes_epoch = sum(w.all_gather_object(
+        sum(spmm_bytes(dp.vplan, r, f)[0] for f in widths for r in dp.local)))
+    op = gr.dm.fwd
+    halo_rows = int(op.counts.sum())
+    aware = sum(halo_rows * f for f in widths)
+    obl = sum((p - 1) * g.n * f for f in widths)
+    exch = None
+    if t_xchg is not None:
+        snd, rcv = [0] * w.size, [0] * w.size
+        for sg in dp.vplan.segments:
+            qs, qd = w.proc_of(sg.src, p), w.proc_of(sg.dst, p)
+            if qs != qd:
+                snd[qs] += sg.count
+                rcv[qd] += sg.count
+        inter = max(max(snd), max(rcv)) * 4 * f0
+        nvl, nvl_src = nvlink_peak()
+        exch = {"bound": "nvlink", "achieved": round(inter / t_xchg / 1e9, 1), "peak": nvl,
+                "unit": "GB/s", "frac": round(inter / t_xchg / 1e9 / nvl, 4),
+                "peak_source": nvl_src, "exchange_ms": round(t_xchg * 1e3, 3),
+                "busiest_rank_bytes": int(inter), "f": f0}
+    cpu = None
+    if lead and not args.no_cpu_baseline:
+        cms, rates, smp = cpu_reference_epoch_ms(sample, wl, budget_s=args.ref_budget,
+                                                 nnz_total=g.nnz_total)
+        cpu = {"value": round(cms, 1), "unit": "ms", "cores": 1, "kind": "port",
+               "sample": smp.replace("leading-row samples",
+                                     f"a {sample.nnz:,}-nnz leading-row sample of block 0 "
+                                     "(columns compacted)") + " -- full-graph estimate"}
+    if not lead:
+        return 0
+    line = {
+        "metric": "gcn_epoch_ms", "value": round(ms_epoch, 3), "unit": "ms",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_epoch, 3), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32 (SpMM accumulates f64)", "data": "synthetic",
+        "config": {"workload": wl["desc"], "variant": args.variant, "p": p, "c": 1,
+                   "partition": "block (partition.py:154-161)",
+                   "l2": "inputs larger than L2 (H0 = %d MB per GPU)"
+                         % (sum(t.numel() for t in gr.x.values()) * 4 // 2**20),
+                   "ranks_per_gpu": args.ranks_per_gpu,
+                   "halo": "single-buffered (one extra device barrier per phase)"},
+        "spmm_hbm_gbs": round(spmm_bytes_epoch / (ms_epoch / 1e3) / 1e9, 1),
+        "comm_elements_per_epoch": {"aware": int(aware), "oblivious": int(obl),
+                                    "ratio": round(aware / obl, 4) if obl else None},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": ncu_traffic(f"papers_f{f0}_p{p}_c1"),
+                     "kernel": "spmm_kernel (layer-1 forward SpMM, f=%d, rank 0)" % f0,
+                     "algorithmic_bytes": int(tot_b), "kernel_ms": round(t_spmm * 1e3, 3),
+                     "gather_gbs": round(gather_b / t_spmm / 1e9, 1), "peak_source": peak_src},
+        "exchange": exch,
+        "e2e": None,
+        "cpu_baseline": cpu,
+        "gpu_launches": int(launches),
+        "epoch_breakdown_ms": breakdown,
+        "peak_mem_gib": round(peak_mem / 2**30, 1),
+        "setup_s": round(t_setup, 1),
+        "clocks": clocks,
+        "loss": [round(v, 6) for v in res.losses.tolist()],
+        "nnz": int(g.nnz_total),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_ours(args, wl):
     import torch
+    if args.workload == "papers":
+        return run_papers(args, wl)
     import paper_2504_04673_b200 as P
     from paper_2504_04673_b200 import _lib
     from paper_2504_04673_b200.dist import world

@@ -60,6 +60,8 @@ int dg_ipc_close(void* dev_ptr);
  * `max_chunk` nonzeros and reduced in a fixed order (deterministic).     */
 typedef struct dg_spmm_plan dg_spmm_plan;
 #define DG_PLAN_SKIP_EMPTY_ROWS 1  /* no work items for rows without entries (z untouched) */
+#define DG_PLAN_DEVICE_SRC 2       /* col_ext / val are DEVICE arrays (row_ptr stays host):
+                                      the entries are laid out on the GPU (graphs built in HBM) */
 int dg_spmm_plan_create(dg_spmm_plan** plan, int n_ranks,
                         const int64_t* n_rows, const int64_t* n_local, const int64_t* nnz,
                         const int64_t* const* row_ptr, const int32_t* const* col_ext,
@@ -86,7 +88,7 @@ int dg_spmm_run(dg_spmm_plan* plan, const float* const* h_local, const float* co
  *      buffer, which may live on a peer GPU (P2P / CUDA-IPC mapped).       */
 typedef struct dg_xchg_plan dg_xchg_plan;
 int dg_xchg_plan_create(dg_xchg_plan** plan, int n_segs, const int32_t* src_local,
-                        const int64_t* count, const int32_t* const* idx /* host or NULL */,
+                        const int64_t* count, const int32_t* const* idx /* host, device or NULL */,
                         const int64_t* src_row0, const int32_t* dst_buf,
                         const int64_t* dst_row0);
 int dg_xchg_plan_destroy(dg_xchg_plan* plan);

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("DG_LIB_PATH", os.path.join(_HERE, "libdgb200.so"))
 DG_MAX_LOCAL = 64
 DG_MAX_GROUP = 64
 DG_PLAN_SKIP_EMPTY_ROWS = 1
+DG_PLAN_DEVICE_SRC = 2
 
 _lock = threading.Lock()
 _lib = None

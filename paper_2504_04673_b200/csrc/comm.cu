@@ -94,7 +94,7 @@ int dg_xchg_plan_create(dg_xchg_plan** out, int n_segs, const int32_t* src_local
     const int32_t* di = nullptr;
     if (idx && idx[s] && count[s]) {
       cudaError_t e = cudaMemcpy(p->idx + off, idx[s], count[s] * sizeof(int32_t),
-                                 cudaMemcpyHostToDevice);
+                                 cudaMemcpyDefault);   // host or device lists (UVA)
       if (e != cudaSuccess) {
         dg_xchg_plan_destroy(p);
         return set_err(DG_ERR_CUDA, std::string("xchg idx copy: ") + cudaGetErrorString(e));

@@ -357,6 +357,40 @@ void choose_config(int chunks, int wmax, int* G_out, int* CPL_out, int* nslabs_o
   *nslabs_out = bestS;
 }
 
+// Device-source plans (DG_PLAN_DEVICE_SRC): the CSR already lives in HBM
+// (graphs built on the GPU, too large to stage through host memory).  The
+// items are still built on the host from row_ptr (O(rows)); the entries are
+// laid out by this kernel, one warp per item.
+struct RelayoutArgs {
+  const int32_t* col[DG_MAX_LOCAL];
+  const float* val[DG_MAX_LOCAL];
+  int2* ent[DG_MAX_LOCAL];
+};
+
+__global__ void relayout_kernel(const Item* __restrict__ items, const int64_t* __restrict__ src_lo,
+                                int64_t n_items, RelayoutArgs a) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t w = warp; w < n_items; w += nw) {
+    const Item it = items[w];
+    const int64_t s = src_lo[w];
+    const int32_t* __restrict__ c = a.col[it.rank] + s;
+    const float* __restrict__ v = a.val[it.rank] + s;
+    int2* __restrict__ d = a.ent[it.rank] + it.lo;
+    for (int32_t k = lane; k < it.len; k += 32) d[k] = make_int2(c[k], __float_as_int(v[k]));
+  }
+}
+
+__global__ void max_col_kernel(const int32_t* __restrict__ col, int64_t n, int* __restrict__ out) {
+  int m = -1;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, col[k]);
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 }  // namespace
 
 struct dg_spmm_plan {
@@ -390,6 +424,7 @@ int dg_spmm_plan_create(dg_spmm_plan** out, int n_ranks, const int64_t* n_rows,
                         const int64_t* const* row_ptr, const int32_t* const* col_ext,
                         const float* const* val, int32_t max_chunk, int32_t flags) {
   const bool skip_empty = (flags & DG_PLAN_SKIP_EMPTY_ROWS) != 0;
+  const bool dev_src = (flags & DG_PLAN_DEVICE_SRC) != 0;
   if (!out || n_ranks < 1 || n_ranks > DG_MAX_LOCAL || max_chunk < 1)
     return set_err(DG_ERR_ARG, "dg_spmm_plan_create: bad args");
   auto* p = new dg_spmm_plan();
@@ -406,7 +441,23 @@ int dg_spmm_plan_create(dg_spmm_plan** out, int n_ranks, const int64_t* n_rows,
       return set_err(DG_ERR_ARG, "dg_spmm_plan_create: rank too large for int32 rows");
     }
     int32_t mx = -1;
-    for (int64_t k = 0; k < nnz[r]; ++k) mx = std::max(mx, col_ext[r][k]);
+    if (dev_src) {
+      int* d_mx = nullptr;
+      cudaError_t e = cudaMalloc(&d_mx, sizeof(int));
+      if (e == cudaSuccess) e = cudaMemcpy(d_mx, &mx, sizeof(int), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess && nnz[r] > 0) {
+        max_col_kernel<<<1184, 256>>>(col_ext[r], nnz[r], d_mx);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaMemcpy(&mx, d_mx, sizeof(int), cudaMemcpyDeviceToHost);
+      if (d_mx) cudaFree(d_mx);
+      if (e != cudaSuccess) {
+        delete p;
+        return set_err(DG_ERR_CUDA, std::string("plan max col: ") + cudaGetErrorString(e));
+      }
+    } else {
+      for (int64_t k = 0; k < nnz[r]; ++k) mx = std::max(mx, col_ext[r][k]);
+    }
     p->ext_rows.push_back((int64_t)mx + 1);
     for (int64_t i = 0; i < n_rows[r]; ++i) {
       const int64_t lo = row_ptr[r][i], hi = row_ptr[r][i + 1];
@@ -436,43 +487,94 @@ int dg_spmm_plan_create(dg_spmm_plan** out, int n_ranks, const int64_t* n_rows,
   std::vector<int64_t> cursor(n_ranks, 0);
   std::vector<int64_t> total(n_ranks, 0);
   for (const Item& it : items) total[it.rank] += (it.len + 1) & ~1LL;
-  std::vector<std::vector<int32_t>> host(n_ranks);
-  for (int r = 0; r < n_ranks; ++r) host[r].assign(2 * std::max<int64_t>(total[r], 2), 0);
-  for (Item& it : items) {
-    const int r = it.rank;
-    const int64_t dst = cursor[r];
-    int32_t* h = host[r].data() + 2 * dst;
-    for (int32_t k = 0; k < it.len; ++k) {
-      h[2 * k] = col_ext[r][it.lo + k];
-      float v = val[r][it.lo + k];
-      std::memcpy(&h[2 * k + 1], &v, 4);
-    }
-    it.lo = dst;
-    cursor[r] += (it.len + 1) & ~1LL;
-  }
-  p->n_items = (int64_t)items.size();
-  p->n_fix = (int64_t)fix.size();
-  p->n_slots = slots;
   auto fail = [&](cudaError_t e, const char* what) {
     dg_spmm_plan_destroy(p);
     return set_err(DG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
   };
-  for (int r = 0; r < n_ranks; ++r) {
-    int4* d = nullptr;
-    const size_t bytes = host[r].size() * sizeof(int32_t);
-    cudaError_t e = cudaMalloc(&d, bytes);
-    if (e != cudaSuccess) return fail(e, "cudaMalloc(entries)");
-    p->ent.push_back(d);
-    e = cudaMemcpy(d, host[r].data(), bytes, cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return fail(e, "cudaMemcpy(entries)");
-    p->dev_bytes += (int64_t)bytes;
-    std::vector<int32_t>().swap(host[r]);
+  if (dev_src) {
+    std::vector<int64_t> src_lo(items.size());
+    for (size_t k = 0; k < items.size(); ++k) {
+      Item& it = items[k];
+      src_lo[k] = it.lo;
+      it.lo = cursor[it.rank];
+      cursor[it.rank] += (it.len + 1) & ~1LL;
+    }
+    RelayoutArgs ra;
+    std::memset(&ra, 0, sizeof(ra));
+    for (int r = 0; r < n_ranks; ++r) {
+      int4* d = nullptr;
+      const size_t bytes = (size_t)std::max<int64_t>(total[r], 2) * 8;
+      cudaError_t e = cudaMalloc(&d, bytes);
+      if (e != cudaSuccess) return fail(e, "cudaMalloc(entries)");
+      p->ent.push_back(d);
+      e = cudaMemset(d, 0, bytes);
+      if (e != cudaSuccess) return fail(e, "cudaMemset(entries)");
+      p->dev_bytes += (int64_t)bytes;
+      ra.col[r] = col_ext[r];
+      ra.val[r] = val[r];
+      ra.ent[r] = reinterpret_cast<int2*>(d);
+    }
+    if (!items.empty()) {
+      Item* d_items = nullptr;
+      int64_t* d_lo = nullptr;
+      cudaError_t e = cudaMalloc(&d_items, items.size() * sizeof(Item));
+      if (e == cudaSuccess) e = cudaMalloc(&d_lo, items.size() * sizeof(int64_t));
+      if (e == cudaSuccess)
+        e = cudaMemcpy(d_items, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice);
+      if (e == cudaSuccess)
+        e = cudaMemcpy(d_lo, src_lo.data(), items.size() * sizeof(int64_t),
+                       cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) {
+        relayout_kernel<<<148 * 16, 256>>>(d_items, d_lo, (int64_t)items.size(), ra);
+        e = cudaGetLastError();
+      }
+      if (e == cudaSuccess) e = cudaDeviceSynchronize();
+      if (d_lo) cudaFree(d_lo);
+      if (e != cudaSuccess) {
+        if (d_items) cudaFree(d_items);
+        return fail(e, "relayout");
+      }
+      p->items = d_items;
+    }
+  } else {
+    std::vector<std::vector<int32_t>> host(n_ranks);
+    for (int r = 0; r < n_ranks; ++r) host[r].assign(2 * std::max<int64_t>(total[r], 2), 0);
+    for (Item& it : items) {
+      const int r = it.rank;
+      const int64_t dst = cursor[r];
+      int32_t* h = host[r].data() + 2 * dst;
+      for (int32_t k = 0; k < it.len; ++k) {
+        h[2 * k] = col_ext[r][it.lo + k];
+        float v = val[r][it.lo + k];
+        std::memcpy(&h[2 * k + 1], &v, 4);
+      }
+      it.lo = dst;
+      cursor[r] += (it.len + 1) & ~1LL;
+    }
+    for (int r = 0; r < n_ranks; ++r) {
+      int4* d = nullptr;
+      const size_t bytes = host[r].size() * sizeof(int32_t);
+      cudaError_t e = cudaMalloc(&d, bytes);
+      if (e != cudaSuccess) return fail(e, "cudaMalloc(entries)");
+      p->ent.push_back(d);
+      e = cudaMemcpy(d, host[r].data(), bytes, cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return fail(e, "cudaMemcpy(entries)");
+      p->dev_bytes += (int64_t)bytes;
+      std::vector<int32_t>().swap(host[r]);
+    }
   }
-  cudaError_t e = cudaMalloc(&p->items, std::max<size_t>(items.size(), 1) * sizeof(Item));
-  if (e != cudaSuccess) return fail(e, "cudaMalloc(items)");
-  if (!items.empty()) {
-    e = cudaMemcpy(p->items, items.data(), items.size() * sizeof(Item), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return fail(e, "cudaMemcpy(items)");
+  p->n_items = (int64_t)items.size();
+  p->n_fix = (int64_t)fix.size();
+  p->n_slots = slots;
+  cudaError_t e = cudaSuccess;
+  if (!p->items) {
+    e = cudaMalloc(&p->items, std::max<size_t>(items.size(), 1) * sizeof(Item));
+    if (e != cudaSuccess) return fail(e, "cudaMalloc(items)");
+    if (!items.empty()) {
+      e = cudaMemcpy(p->items, items.data(), items.size() * sizeof(Item),
+                     cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return fail(e, "cudaMemcpy(items)");
+    }
   }
   e = cudaMalloc(&p->fix, std::max<size_t>(fix.size(), 1) * sizeof(Fixup));
   if (e != cudaSuccess) return fail(e, "cudaMalloc(fix)");

@@ -71,18 +71,33 @@ def _stream():
     return L.stream_ptr()
 
 
+def _ptr(a):
+    return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+
+
+def _numel(a):
+    return a.numel() if isinstance(a, torch.Tensor) else a.size
+
+
 def _make_spmm_plan(rank_ops, max_chunk, flags=0):
     """dg_spmm_plan over a list of RankOperand-like objects (row_ptr,
-    col_ext, val, n_rows, n_local)."""
+    col_ext, val, n_rows, n_local).  col_ext / val may be CUDA tensors (a
+    graph built in HBM): the entries are then laid out on the device."""
     lib = L.lib()
     n = len(rank_ops)
+    dev = [isinstance(x.col_ext, torch.Tensor) for x in rank_ops]
+    if any(dev):
+        if not all(dev):
+            raise ValueError("mixed host / device operands in one plan")
+        flags |= L.DG_PLAN_DEVICE_SRC
+        torch.cuda.synchronize()
     rp = (C.c_void_p * n)(*[x.row_ptr.ctypes.data for x in rank_ops])
-    ce = (C.c_void_p * n)(*[x.col_ext.ctypes.data for x in rank_ops])
-    va = (C.c_void_p * n)(*[x.val.ctypes.data for x in rank_ops])
+    ce = (C.c_void_p * n)(*[_ptr(x.col_ext) for x in rank_ops])
+    va = (C.c_void_p * n)(*[_ptr(x.val) for x in rank_ops])
     h = C.c_void_p()
     L.check(lib.dg_spmm_plan_create(C.byref(h), n, L.i64_array([x.n_rows for x in rank_ops]),
                                     L.i64_array([x.n_local for x in rank_ops]),
-                                    L.i64_array([x.col_ext.size for x in rank_ops]),
+                                    L.i64_array([_numel(x.col_ext) for x in rank_ops]),
                                     rp, ce, va, max_chunk, flags))
     return h
 
@@ -95,20 +110,24 @@ def _check_bounds(vplan, local):
     destination halo."""
     for r in local:
         ro = vplan.ranks[r]
-        if ro.col_ext.size:
+        if _numel(ro.col_ext):
             lo, hi = int(ro.col_ext.min()), int(ro.col_ext.max())
             if lo < 0 or hi >= ro.n_local + ro.halo_rows:
                 raise ValueError(f"rank {r}: extended column {lo}..{hi} outside "
                                  f"[0, {ro.n_local + ro.halo_rows})")
-        if ro.row_ptr[0] != 0 or ro.row_ptr[-1] != ro.col_ext.size or \
+        if ro.row_ptr[0] != 0 or ro.row_ptr[-1] != _numel(ro.col_ext) or \
                 np.any(np.diff(ro.row_ptr) < 0):
             raise ValueError(f"rank {r}: malformed row pointers")
     widths = getattr(vplan, "widths", None)
     for sg in vplan.segments:
         if sg.dst_row0 < 0 or sg.dst_row0 + sg.count > vplan.ranks[sg.dst].halo_rows:
             raise ValueError(f"segment {sg.src}->{sg.dst} overflows the receiver's halo")
-        if sg.idx is not None and sg.idx.size and (int(sg.idx.min()) < 0 or
-                                                   int(sg.idx.max()) >= widths[sg.q]):
+        if sg.src not in local:
+            continue                                   # sent by another process
+        if sg.idx is not None and _numel(sg.idx) != sg.count:
+            raise ValueError(f"segment {sg.src}->{sg.dst}: row list length != count")
+        if sg.idx is not None and _numel(sg.idx) and (int(sg.idx.min()) < 0 or
+                                                      int(sg.idx.max()) >= widths[sg.q]):
             raise ValueError(f"segment {sg.src}->{sg.dst} indexes outside block {sg.q}")
         if sg.idx is None and sg.count > widths[sg.q]:
             raise ValueError(f"segment {sg.src}->{sg.dst} longer than block {sg.q}")
@@ -120,9 +139,18 @@ class _Part:
 
     def __init__(self, ro, boundary):
         keep = (ro.col_ext >= ro.n_local) if boundary else (ro.col_ext < ro.n_local)
-        rows = np.repeat(np.arange(ro.n_rows, dtype=np.int64), np.diff(ro.row_ptr))[keep]
         self.n_rows, self.n_local = ro.n_rows, ro.n_local
         self.row_ptr = np.zeros(ro.n_rows + 1, dtype=np.int64)
+        if isinstance(ro.col_ext, torch.Tensor):       # operand resident in HBM
+            lens = torch.from_numpy(np.diff(ro.row_ptr)).to(ro.col_ext.device)
+            rows = torch.repeat_interleave(torch.arange(ro.n_rows, device=lens.device), lens)
+            cnt = torch.bincount(rows[keep], minlength=ro.n_rows)
+            del rows, lens
+            self.row_ptr[1:] = torch.cumsum(cnt, 0).cpu().numpy()
+            self.col_ext = ro.col_ext[keep].contiguous()
+            self.val = ro.val[keep].contiguous()
+            return
+        rows = np.repeat(np.arange(ro.n_rows, dtype=np.int64), np.diff(ro.row_ptr))[keep]
         if rows.size:
             np.cumsum(np.bincount(rows, minlength=ro.n_rows), out=self.row_ptr[1:])
         self.col_ext = np.ascontiguousarray(ro.col_ext[keep])
@@ -143,7 +171,7 @@ class DevicePlan:
     pass that accumulates into Z once the barrier has passed."""
 
     def __init__(self, vplan, local_ranks=None, acc=ACC_FP64, max_chunk=MAX_CHUNK, max_ld=None,
-                 standalone=False):
+                 standalone=False, parities=2):
         from .dist import world
         lib = L.lib()
         self.vplan = vplan
@@ -154,6 +182,13 @@ class DevicePlan:
         self.local = list(range(vplan.grid.p)) if local_ranks is None else list(local_ranks)
         self.li = {r: k for k, r in enumerate(self.local)}
         self.acc = acc
+        # halo parities (multi-process): 2 = double-buffered (one device
+        # barrier per phase); 1 = single buffer, one more barrier before the
+        # exchange overwrites it (halves the halo memory of graphs whose halos
+        # fill HBM, e.g. the papers-shaped config)
+        if parities not in (1, 2):
+            raise ValueError("parities must be 1 or 2")
+        self.parities = parities
         self.device = torch.device("cuda", torch.cuda.current_device())
         ro = [vplan.ranks[r] for r in self.local]
         _check_bounds(vplan, self.local)
@@ -180,7 +215,7 @@ class DevicePlan:
         L.check(lib.dg_xchg_plan_create(
             C.byref(xh), len(segs), L.i32_array([self.li[s.src] for s in segs]),
             L.i64_array([s.count for s in segs]),
-            (C.c_void_p * max(len(segs), 1))(*[0 if s.idx is None else s.idx.ctypes.data
+            (C.c_void_p * max(len(segs), 1))(*[0 if s.idx is None else _ptr(s.idx)
                                                for s in segs]),
             L.i64_array([0] * len(segs)), L.i32_array([s.dst for s in segs]),
             L.i64_array([s.dst_row0 for s in segs])))
@@ -193,6 +228,17 @@ class DevicePlan:
         info = (C.c_int64 * 8)()
         L.check(lib.dg_spmm_plan_info(self._splan, info))
         self.info = list(info)
+        for x in ro:
+            if isinstance(x.col_ext, torch.Tensor):
+                # HBM-resident operand: the plans hold their own copy of the
+                # entries; keep only the counts (frees ~8 B per nonzero)
+                x.nnz = int(x.col_ext.numel())
+                occ = torch.zeros(x.n_local + x.halo_rows + 1, dtype=torch.bool,
+                                  device=self.device)
+                occ[x.col_ext.long()] = True
+                x.u = int(occ.sum())
+                del occ
+                x.col_ext = x.val = None
         if self.multi:
             self._init_symmetric(max_ld)
 
@@ -211,7 +257,7 @@ class DevicePlan:
         for r in range(p):
             q = w.proc_of(r, p)
             self._hoff[r] = hsize[q]
-            hsize[q] += 2 * ranks[r].halo_rows * self.max_ld * 4
+            hsize[q] += self.parities * ranks[r].halo_rows * self.max_ld * 4
             self._poff[r] = psize[q]
             psize[q] += 2 * ranks[r].n_rows * self.max_ld * 4 if self.reduce else 0
         self.hsym = SymBuffer(w, max(hsize[w.proc], 16))
@@ -220,7 +266,7 @@ class DevicePlan:
     def _halo_ptr(self, r, par):
         q = self.world.proc_of(r, self.grid.p)
         return (self.hsym.ptrs[q] + self._hoff[r]
-                + par * self.vplan.ranks[r].halo_rows * self.max_ld * 4)
+                + (par % self.parities) * self.vplan.ranks[r].halo_rows * self.max_ld * 4)
 
     def _partial_ptr(self, r, par):
         q = self.world.proc_of(r, self.grid.p)
@@ -321,6 +367,10 @@ class DevicePlan:
         main = torch.cuda.current_stream()
         self._side.wait_stream(main)                    # H is ready
         with torch.cuda.stream(self._side):
+            if self.parities == 1:
+                # every peer has finished reading its (single) halo buffer
+                # in the previous phase before anyone overwrites it
+                self.world.barrier()
             self._xchg(hs, dst, f, ld, L.stream_ptr(self._side))
             self.world.barrier()                        # every peer's rows have landed
         zp = ([self._partial_ptr(r, par) for r in self.local] if self.reduce

@@ -356,13 +356,17 @@ class GcnRun:
         for op in {id(self.dm.fwd): self.dm.fwd, id(self.dm.bwd): self.dm.bwd}.values():
             device_plan(op, grid, cfg.variant, max_ld=max(self.lds))
 
+    def _inputs(self, i):
+        """Block row i of the features, labels and mask (device views)."""
+        r0, r1 = self.dm.boundaries[i]
+        return self.x[r0:r1], self.labels[r0:r1], self.mask[r0:r1]
+
     def program(self, comm, epochs, stats, weights_out=None):
         """The per-rank epoch loop (gcn.py:258-286)."""
         cfg, dm = self.cfg, self.dm
         i, j = comm.coords
         r0, r1 = dm.boundaries[i]
-        h0 = self.x[r0:r1]
-        yb, mb = self.labels[r0:r1], self.mask[r0:r1]
+        h0, yb, mb = self._inputs(i)
         ws = [w.clone() for w in self.w0] if weights_out is None else weights_out
         xent = self.xent.setdefault(comm.rank, _Xent(r1 - r0, self.device))
         dense = self.dense.setdefault(comm.rank, _Dense(self.device))
@@ -414,6 +418,7 @@ class GcnRun:
                 g = torch.empty_like(logits)
                 xent(logits, dims[-1], yb, mb, self.denom, g, stats[epoch])
                 mark("xent")
+                hs[-1] = zs[-1] = logits = None       # not needed by the backward pass
                 for l in range(last, -1, -1):
                     m = spmm_phase(comm, dm.bwd, g, dims[l + 1], cfg.variant)
                     mark(f"bwd_spmm_f{dims[l + 1]}")

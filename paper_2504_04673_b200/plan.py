@@ -217,6 +217,8 @@ def build_variant_plan(op: DistOperand, grid: ProcessGrid, variant: str,
     """Plan of `variant` on `grid`.  The halo layout and exchange segments
     are computed for every rank (every process needs its peers' offsets);
     the remapped CSR only for `local_ranks` (default: all)."""
+    if hasattr(op, "build_variant_plan"):          # HBM-resident operand (sharded.py)
+        return op.build_variant_plan(grid, variant, local_ranks)
     validate_variant_grid(variant, grid.p, grid.c)
     hosted = set(range(grid.p)) if local_ranks is None else set(local_ranks)
     aware = variant.endswith("sparse")

@@ -60,7 +60,8 @@ def device_plan(op: DistOperand, grid: ProcessGrid, variant: str, max_ld=None):
     if dp is not None and w.multi and max_ld is not None and max_ld > dp.max_ld:
         raise ValueError(f"row pitch {max_ld} exceeds this plan's registered {dp.max_ld}")
     if dp is None:
-        dp = DevicePlan(build_variant_plan(op, grid, variant, local), local, max_ld=max_ld)
+        dp = DevicePlan(build_variant_plan(op, grid, variant, local), local, max_ld=max_ld,
+                        parities=getattr(op, "parities", 2))
         op._device[key] = dp
     return dp
 

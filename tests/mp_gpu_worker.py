@@ -87,6 +87,43 @@ def main():
                     if not np.array_equal(w0, wr):
                         fails.append((key, "reduce_after_transform replication"))
             n_checked += 1
+    # HBM-resident sharded path (sharded.py): each process builds only its
+    # block rows; single-buffered halos; must equal the host-plan GcnRun
+    import torch
+    from paper_2504_04673_b200 import graphgen, sharded
+    a = P.gcn_normalize(graphgen.rmat(11, 8, 5))
+    a.values = a.values.astype(np.float32).astype(np.float64)
+    for p in sorted({w.size, 2 * w.size}):
+        f_in, classes = 40, 9
+        cfg = P.TrainConfig(layers=3, hidden=16, lr=0.1, epochs=3, seed=2, variant="1d-sparse")
+        sg = sharded.ShardedGraph.from_csr(a, p)
+        x, y = sharded.sharded_inputs(sg, f_in, classes, seed=4)
+        gr = sharded.sharded_gcn_run(sg, x, y, f_in, classes, cfg)
+        res = gr.result(gr.run())
+        gr.close()
+        # host reference: the full inputs, assembled from every process's blocks
+        xs = w.all_gather_object({i: t[:, :f_in].cpu().numpy() for i, t in x.items()})
+        ys = w.all_gather_object({i: t.cpu().numpy() for i, t in y.items()})
+        xd, yd = {}, {}
+        for d in xs:
+            xd.update(d)
+        for d in ys:
+            yd.update(d)
+        xf = np.concatenate([xd[i] for i in range(p)])
+        yf = np.concatenate([yd[i] for i in range(p)])
+        ref = P.train(a, xf, yf, np.ones(a.n_rows, bool), cfg, p=p)
+        if not np.array_equal(res.losses, ref.losses):
+            fails.append(("sharded", p, "loss", res.losses.tolist(), ref.losses.tolist()))
+        for w1, w2 in zip(res.weights, ref.weights):
+            if not np.array_equal(w1, w2):
+                fails.append(("sharded", p, "weights"))
+        for prim in ref.ledger.counters:
+            for name, v in ref.ledger.counters[prim].items():
+                if not np.array_equal(res.ledger.counters[prim][name], v):
+                    fails.append(("sharded", p, "ledger", prim, name))
+        n_checked += 1
+        del x, y, sg
+        torch.cuda.empty_cache()
     print(f"[proc {w.proc}/{w.size}] checked {n_checked} cases, {len(fails)} failures",
           flush=True)
     for f in fails:
