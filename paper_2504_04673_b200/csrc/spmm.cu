@@ -27,6 +27,8 @@
 
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace {
 
 struct Item {          // 24 B: one row, or one fixed chunk of a long row
@@ -130,8 +132,8 @@ struct Vec<8> {
   }
 };
 
-template <int G, int CPL, bool F64, int V>
-__global__ void __launch_bounds__(256, (Tune<CPL, V>::MINB))
+template <int G, int CPL, bool F64, int V, int MB = Tune<CPL, V>::MINB>
+__global__ void __launch_bounds__(256, MB)
     spmm_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int E = Tune<CPL, V>::E;        // entries per pipeline step
   constexpr int E4 = E / 2;                 // int4 loads per step
@@ -308,11 +310,11 @@ int bucket_of(int32_t len) {
   return (int)(4.0 * std::log2((double)len)) + 1;
 }
 
-template <int G, int CPL, bool F64, int V>
+template <int G, int CPL, bool F64, int V, int MB = Tune<CPL, V>::MINB>
 void launch_spmm(const SpmmArgs& a, int nslabs, cudaStream_t s) {
   const int64_t threads = a.n_items * G;
   const unsigned gx = (unsigned)((threads + 255) / 256);
-  spmm_kernel<G, CPL, F64, V><<<dim3(gx, nslabs), 256, 0, s>>>(a);
+  spmm_kernel<G, CPL, F64, V, MB><<<dim3(gx, nslabs), 256, 0, s>>>(a);
 }
 
 using LaunchFn = void (*)(const SpmmArgs&, int, cudaStream_t);
@@ -327,6 +329,23 @@ LaunchFn pick_launch(int G, int CPL) {
   DG_CASE(8, 1) DG_CASE(8, 2) DG_CASE(8, 3) DG_CASE(8, 4)
   DG_CASE(16, 1) DG_CASE(16, 2) DG_CASE(16, 3) DG_CASE(16, 4)
   DG_CASE(32, 1) DG_CASE(32, 2) DG_CASE(32, 3) DG_CASE(32, 4)
+#undef DG_CASE
+  return nullptr;
+}
+
+// Tuning overrides for sweeps (scripts/spmm_sweep.py): DG_SPMM_MINB=3|4
+// raises the CTAs-per-SM target of the one-chunk-per-lane 256-bit fp64
+// kernels; DG_SPMM_FORCE="G,CPL" fixes the lane shape.  Read once.
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+LaunchFn pick_minb(int G, int MB) {
+#define DG_CASE(g, m) \
+  if (G == g && MB == m) return &launch_spmm<g, 1, true, 8, m>;
+  DG_CASE(2, 3) DG_CASE(4, 3) DG_CASE(8, 3) DG_CASE(16, 3) DG_CASE(32, 3)
+  DG_CASE(2, 4) DG_CASE(4, 4) DG_CASE(8, 4) DG_CASE(16, 4) DG_CASE(32, 4)
 #undef DG_CASE
   return nullptr;
 }
@@ -656,6 +675,14 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   }
   int G, CPL, ns;
   choose_config(chunks, wmax, &G, &CPL, &ns);
+  static const int force_g = env_int("DG_SPMM_FORCE_G", 0);
+  static const int force_c = env_int("DG_SPMM_FORCE_CPL", 0);
+  static const int minb = env_int("DG_SPMM_MINB", 0);
+  if (force_g > 0 && force_c > 0) {
+    G = force_g;
+    CPL = force_c;
+    ns = (chunks + G * CPL - 1) / (G * CPL);
+  }
   a.items = p->items;
   a.part = p->part;
   a.n_items = p->n_items;
@@ -668,6 +695,7 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   if (p->n_items == 0) return DG_OK;
   LaunchFn fn = v8 ? (acc ? pick_launch<true, 8>(G, CPL) : pick_launch<false, 8>(G, CPL))
                    : (acc ? pick_launch<true, 4>(G, CPL) : pick_launch<false, 4>(G, CPL));
+  if (v8 && acc && CPL == 1 && minb >= 3) fn = pick_minb(G, minb);
   if (!fn) return set_err(DG_ERR_ARG, "dg_spmm_run: no kernel for config");
   fn(a, ns, S(stream));
   DG_LAUNCHED();

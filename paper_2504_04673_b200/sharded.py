@@ -126,7 +126,7 @@ def chung_lu_sharded(n, pairs, p, alpha=0.6, max_weight=None, seed=0, world=None
     cdf = cdf / cdf[-1]
     del wt
     keys = torch.zeros(0, dtype=torch.int64, device=dev)
-    draw = int(pairs * 1.02) + 4096
+    draw = pairs                   # duplicates / self-pairs are topped up below
     total = 0
     while True:
         kept = [keys]
@@ -152,7 +152,7 @@ def chung_lu_sharded(n, pairs, p, alpha=0.6, max_weight=None, seed=0, world=None
         say(f"[sharded] distinct pairs {total:,} of {pairs:,}")
         if total >= pairs:
             break
-        draw = int((pairs - total) * 1.25) + 4096
+        draw = int((pairs - total) * 1.05) + 1024
     del cdf
     # ---- block rows: entries (lo, hi) for lo in the block, (hi, lo) for hi
     blocks, deg_local = {}, {}
