@@ -92,7 +92,10 @@ template <int CPL, int V>
 struct Tune {
   static constexpr int E = 4;                       // entries per pipeline step
   static constexpr int W = CPL * V / 4;             // float4s per lane
-  static constexpr int MINB = W == 1 ? 4 : (W == 2 ? 2 : 1);
+  // one 256-bit chunk per lane: 3 CTAs/SM (80 registers) -- more warps in
+  // flight beat a 12-byte spill (sweep, profiles/r01/spmm_sweep_minb.txt:
+  // f=602 24.4 -> 19.8 ms, f=100 4.8 -> 4.0 ms; 4 CTAs/SM spill 80 B: slower)
+  static constexpr int MINB = W == 1 ? 4 : (CPL == 1 && V == 8 ? 3 : (W == 2 ? 2 : 1));
 };
 
 // V floats per lane-chunk: 4 -> 128-bit loads (LDG.128); 8 -> Blackwell's
