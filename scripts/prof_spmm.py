@@ -28,11 +28,18 @@ def main():
     ap.add_argument("--slab", type=int, nargs="+", default=[0])
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--ld-align", type=int, default=0)
+    ap.add_argument("--community", action="store_true",
+                    help="products: community-ordered layout (as bench.py uses)")
     ap.add_argument("--cusparse", action="store_true",
                     help="also time torch.sparse.mm (cuSPARSE) on the same matrix (comparator)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     a = bench.make_graph(args.workload)
+    if args.community and args.workload in bench._COMM:
+        from paper_2504_04673_b200.graphgen import community_partition
+        part = community_partition(bench._COMM[args.workload], 1)
+        a, _ = P.apply_partition(a, None, part)
+        print("community-ordered layout", flush=True)
     grid = P.ProcessGrid(1, 1)
     dm = P.build_dist_matrices(a, [(0, a.n_rows)], grid)
     if args.chunk:
