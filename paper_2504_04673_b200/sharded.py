@@ -89,6 +89,31 @@ class ShardedGraph:
         self.blocks = {i: None for i in self.blocks}
 
 
+def _s64(c):
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+_GOLD, _MIX1, _MIX2 = _s64(0x9E3779B97F4A7C15), _s64(0xBF58476D1CE4E5B9), _s64(0x94D049BB133111EB)
+
+
+def _splitmix64(x):
+    """splitmix64 finaliser on int64 tensors (two's-complement wraparound;
+    logical shifts by masking): a counter-based generator whose output is a
+    pure function of the index -- identical on every device and process,
+    whatever the chunking."""
+    z = x * _GOLD + _GOLD
+    z = (z ^ ((z >> 30) & ((1 << 34) - 1))) * _MIX1
+    z = (z ^ ((z >> 27) & ((1 << 37) - 1))) * _MIX2
+    return z ^ ((z >> 31) & ((1 << 33) - 1))
+
+
+def _uniform(seed, stream, start, m, dev):
+    """m uniform doubles in [0, 1): draws start .. start+m-1 of `stream`."""
+    k = torch.arange(start, start + m, device=dev, dtype=torch.int64)
+    z = _splitmix64(_splitmix64(k * 4 + stream) ^ int(seed))
+    return ((z >> 11) & ((1 << 53) - 1)).to(torch.float64) * (2.0 ** -53)
+
+
 def _all_gather_np(w, arr):
     return [np.asarray(x) for x in w.all_gather_object(arr)]
 
@@ -113,31 +138,30 @@ def chung_lu_sharded(n, pairs, p, alpha=0.6, max_weight=None, seed=0, world=None
     bounds, starts = block_bounds(n, p)
     hosted = w.local_ranks(p) if w.multi else list(range(p))
     R0, R1 = bounds[hosted[0]][0], bounds[hosted[-1]][1]
-    g = torch.Generator(device=dev)
-    g.manual_seed(int(seed))
     wt = (torch.arange(n, device=dev, dtype=torch.float64) + 1.0) ** (-alpha)
     wt = wt / wt.sum() * (2.0 * pairs)
     if max_weight is not None:
         for _ in range(8):
             wt = torch.clamp(wt, max=float(max_weight))
             wt = wt / wt.sum() * (2.0 * pairs)
-    wt = wt[torch.randperm(n, generator=g, device=dev)]
+    # seeded relabel (hubs scattered): a permutation from sorting hashed ids
+    wt = wt[torch.argsort(_splitmix64(torch.arange(n, device=dev) * 4 + 3) ^ int(seed))]
     cdf = torch.cumsum(wt, 0)
     cdf = cdf / cdf[-1]
     del wt
     keys = torch.zeros(0, dtype=torch.int64, device=dev)
     draw = pairs                   # duplicates / self-pairs are topped up below
     total = 0
+    drawn = 0                      # draws consumed so far (counter of the generator)
     while True:
         kept = [keys]
         todo = draw
         while todo > 0:
             m = min(_CHUNK, todo)
             todo -= m
-            u = torch.searchsorted(cdf, torch.rand(m, generator=g, device=dev,
-                                                   dtype=torch.float64))
-            v = torch.searchsorted(cdf, torch.rand(m, generator=g, device=dev,
-                                                   dtype=torch.float64))
+            u = torch.searchsorted(cdf, _uniform(seed, 0, drawn, m, dev))
+            v = torch.searchsorted(cdf, _uniform(seed, 1, drawn, m, dev))
+            drawn += m
             u.clamp_(max=n - 1)
             v.clamp_(max=n - 1)
             lo, hi = torch.minimum(u, v), torch.maximum(u, v)
@@ -149,6 +173,8 @@ def chung_lu_sharded(n, pairs, p, alpha=0.6, max_weight=None, seed=0, world=None
         del kept
         owned = int(((keys >= R0 * n) & (keys < R1 * n)).sum())
         total = sum(w.all_gather_object(owned))
+        if w.multi:
+            _check_cross_pairs(w, keys, n, p, bounds)
         say(f"[sharded] distinct pairs {total:,} of {pairs:,}")
         if total >= pairs:
             break
@@ -207,6 +233,31 @@ def chung_lu_sharded(n, pairs, p, alpha=0.6, max_weight=None, seed=0, world=None
     nnz_total = sum(w.all_gather_object(nnz_local))
     torch.cuda.empty_cache()
     return ShardedGraph(n, p, blocks, nnz_total, w)
+
+
+def _check_cross_pairs(w, keys, n, p, bounds):
+    """Every pair joining two processes' rows is held by both: the number of
+    (lo in A, hi in B) pairs each process holds must agree (a cheap guard
+    against the processes drawing different graphs)."""
+    size = w.size
+    edges = torch.tensor([bounds[r][0] for r in range(p) if w.proc_of(r, p) != w.proc_of(r - 1, p)
+                          or r == 0] + [n], device=keys.device, dtype=torch.int64)
+    cnt = torch.zeros((size, size), dtype=torch.int64, device=keys.device)
+    for c0 in range(0, keys.numel(), _CHUNK):
+        kc = keys[c0:c0 + _CHUNK]
+        a = torch.searchsorted(edges, kc // n, right=True) - 1
+        b = torch.searchsorted(edges, kc % n, right=True) - 1
+        cnt += torch.bincount(a * size + b, minlength=size * size).view(size, size)
+    mine = cnt.cpu().numpy()
+    allc = w.all_gather_object(mine)
+    me = w.proc
+    for q in range(size):
+        if q == me:
+            continue
+        a, b = min(me, q), max(me, q)
+        if allc[me][a, b] != allc[q][a, b]:
+            raise RuntimeError(f"processes {me} and {q} drew different graphs "
+                               f"({allc[me][a, b]} vs {allc[q][a, b]} shared pairs)")
 
 
 def papers_shaped_sharded(p, seed=0, n=111_059_956, nnz=3_231_371_744, world=None, log=None):

@@ -116,3 +116,76 @@ def test_chung_lu_sharded_normalised_symmetric_cpu(cpu_dev, p):
     assert np.array_equal(ref.col_idx, full.col_idx)
     assert np.array_equal(ref.values.astype(np.float32), val)
     assert P.csr_equal(P.transpose_csr(full), full)
+
+
+class _Shared:
+    def __init__(self, size):
+        import threading
+        self.size, self.bar, self.slots = size, threading.Barrier(size), [None] * size
+
+
+class _ProcView:
+    """One simulated process of a `size`-process world (threads stand in
+    for processes; all_gather_object through a barrier)."""
+
+    multi = True
+
+    def __init__(self, sh, proc):
+        self.sh, self.proc, self.size = sh, proc, sh.size
+
+    def all_gather_object(self, obj):
+        self.sh.bar.wait()
+        self.sh.slots[self.proc] = obj
+        self.sh.bar.wait()
+        out = list(self.sh.slots)
+        self.sh.bar.wait()
+        return out
+
+    def proc_of(self, r, p):
+        return (r * self.size) // p
+
+    def local_ranks(self, p):
+        return [r for r in range(p) if self.proc_of(r, p) == self.proc]
+
+    def init(self):
+        return self
+
+
+@pytest.mark.parametrize("size,p", [(2, 4), (3, 3)])
+def test_chung_lu_sharded_multiprocess_same_graph(cpu_dev, size, p):
+    """Every process draws the same graph (counter-based generator) and
+    keeps only its rows; the union equals the one-process graph, and the
+    sharded operands pass the sender/receiver cross-check."""
+    import threading
+    n, pairs = 2500, 15_000
+    one = sharded.chung_lu_sharded(n, pairs, p, alpha=0.7, max_weight=300, seed=3,
+                                   world=_OneProc())
+    sh = _Shared(size)
+    res, errs = [None] * size, []
+
+    def run(q):
+        try:
+            g = sharded.chung_lu_sharded(n, pairs, p, alpha=0.7, max_weight=300, seed=3,
+                                         world=_ProcView(sh, q))
+            res[q] = (g, sharded.ShardedOperand(g))
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=run, args=(q,)) for q in range(size)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    got = {}
+    for g, _ in res:
+        got.update(g.blocks)
+        assert g.nnz_total == one.nnz_total
+    assert sorted(got) == list(range(p))
+    for i in range(p):
+        assert np.array_equal(got[i][0], one.blocks[i][0])
+        assert torch.equal(got[i][1], one.blocks[i][1])
+        assert torch.equal(got[i][2], one.blocks[i][2])
+    op1 = sharded.ShardedOperand(one)
+    for _, op in res:
+        assert np.array_equal(op.counts, op1.counts)
