@@ -166,6 +166,11 @@ def sbm(n, blocks=2, p_in=0.2, p_out=0.01, seed=0, feature_dim=16, feature_scale
 # large shaped graphs, generated on the GPU (benchmark input synthesis)
 # ---------------------------------------------------------------------------
 
+def _host_cumsum(t):
+    import torch
+    return torch.from_numpy(np.cumsum(t.cpu().numpy())).to(t.device)
+
+
 def chung_lu_device(n, pairs, alpha=0.6, max_weight=None, seed=0, communities=0, p_in=0.8,
                     return_communities=False):
     """Power-law (Chung-Lu) symmetric 0/1 graph with exactly `pairs`
@@ -187,14 +192,17 @@ def chung_lu_device(n, pairs, alpha=0.6, max_weight=None, seed=0, communities=0,
             w = torch.clamp(w, max=float(max_weight))
             w = w / w.sum() * (2.0 * pairs)
     w = w[torch.randperm(n, generator=g, device=dev)]
-    cdf = torch.cumsum(w, 0)
+    # CDFs by a sequential host sum: a parallel GPU scan's float association
+    # depends on timing, and under torchrun every process must draw the
+    # identical graph
+    cdf = _host_cumsum(w)
     cdf = cdf / cdf[-1]
     if communities:
         comm = torch.randint(0, communities, (n,), generator=g, device=dev)
         order = torch.argsort(comm, stable=True)
         cstart = torch.searchsorted(comm[order], torch.arange(communities + 1, device=dev))
         wc = w[order]
-        ccdf = torch.cumsum(wc, 0)
+        ccdf = _host_cumsum(wc)
     keys = torch.zeros(0, dtype=torch.int64, device=dev)
     while keys.numel() < pairs:
         m = int((pairs - keys.numel()) * 1.3) + 4096

@@ -138,16 +138,22 @@ def chung_lu_sharded(n, pairs, p, alpha=0.6, max_weight=None, seed=0, world=None
     bounds, starts = block_bounds(n, p)
     hosted = w.local_ranks(p) if w.multi else list(range(p))
     R0, R1 = bounds[hosted[0]][0], bounds[hosted[-1]][1]
-    wt = (torch.arange(n, device=dev, dtype=torch.float64) + 1.0) ** (-alpha)
+    # degree weights and their CDF on the host: a sequential (numpy) sum is
+    # bit-identical in every process, a parallel GPU scan is not (its
+    # association order depends on timing), and a draw landing on a CDF
+    # boundary would then pick different vertices in different processes
+    wt = (np.arange(n, dtype=np.float64) + 1.0) ** (-alpha)
     wt = wt / wt.sum() * (2.0 * pairs)
     if max_weight is not None:
         for _ in range(8):
-            wt = torch.clamp(wt, max=float(max_weight))
+            wt = np.minimum(wt, float(max_weight))
             wt = wt / wt.sum() * (2.0 * pairs)
     # seeded relabel (hubs scattered): a permutation from sorting hashed ids
-    wt = wt[torch.argsort(_splitmix64(torch.arange(n, device=dev) * 4 + 3) ^ int(seed))]
-    cdf = torch.cumsum(wt, 0)
-    cdf = cdf / cdf[-1]
+    perm = torch.argsort(_splitmix64(torch.arange(n, device=dev) * 4 + 3) ^ int(seed))
+    wt = wt[perm.cpu().numpy()]
+    del perm
+    cdf = np.cumsum(wt)
+    cdf = torch.from_numpy(cdf / cdf[-1]).to(dev)
     del wt
     keys = torch.zeros(0, dtype=torch.int64, device=dev)
     draw = pairs                   # duplicates / self-pairs are topped up below
@@ -242,22 +248,26 @@ def _check_cross_pairs(w, keys, n, p, bounds):
     size = w.size
     edges = torch.tensor([bounds[r][0] for r in range(p) if w.proc_of(r, p) != w.proc_of(r - 1, p)
                           or r == 0] + [n], device=keys.device, dtype=torch.int64)
-    cnt = torch.zeros((size, size), dtype=torch.int64, device=keys.device)
+    cnt = torch.zeros(size * size, dtype=torch.int64, device=keys.device)
+    hsum = torch.zeros(size * size, dtype=torch.int64, device=keys.device)
     for c0 in range(0, keys.numel(), _CHUNK):
         kc = keys[c0:c0 + _CHUNK]
         a = torch.searchsorted(edges, kc // n, right=True) - 1
         b = torch.searchsorted(edges, kc % n, right=True) - 1
-        cnt += torch.bincount(a * size + b, minlength=size * size).view(size, size)
-    mine = cnt.cpu().numpy()
+        ab = a * size + b
+        cnt += torch.bincount(ab, minlength=size * size)
+        # order-independent checksum of the pair set (wrapping int64 sum of hashes)
+        hsum.index_add_(0, ab, _splitmix64(kc))
+    mine = (cnt.cpu().numpy().reshape(size, size), hsum.cpu().numpy().reshape(size, size))
     allc = w.all_gather_object(mine)
     me = w.proc
     for q in range(size):
         if q == me:
             continue
         a, b = min(me, q), max(me, q)
-        if allc[me][a, b] != allc[q][a, b]:
+        if allc[me][0][a, b] != allc[q][0][a, b] or allc[me][1][a, b] != allc[q][1][a, b]:
             raise RuntimeError(f"processes {me} and {q} drew different graphs "
-                               f"({allc[me][a, b]} vs {allc[q][a, b]} shared pairs)")
+                               f"({allc[me][0][a, b]} vs {allc[q][0][a, b]} shared pairs)")
 
 
 def papers_shaped_sharded(p, seed=0, n=111_059_956, nnz=3_231_371_744, world=None, log=None):
