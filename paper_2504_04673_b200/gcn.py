@@ -415,6 +415,7 @@ class GcnRun:
                     hs.append(h if l < last else z)
                     mark(f"fwd_dense_{l}")
                 logits = hs[-1]
+                t = u = parts = z = h = None      # only hs / zs stay alive (HBM at scale)
                 g = torch.empty_like(logits)
                 xent(logits, dims[-1], yb, mb, self.denom, g, stats[epoch])
                 mark("xent")
