@@ -202,7 +202,10 @@ __global__ void __launch_bounds__(256) xent_vec_kernel(
       xl = grp_sum<G>(xl);
       am = grp_min<G>(am);
       const bool on = valid[u] && mask[row] != 0;
-      const double inv_s = 1.0 / s;
+      // (softmax - onehot) / denom with one division per row: p_j/denom =
+      // e_j * (1 / (s * denom)); the label term subtracts 1/denom
+      const double scale = 1.0 / (s * denom);
+      const double inv_d = 1.0 / denom;
       float4* gr = reinterpret_cast<float4*>(grad + row * ldg);
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -212,9 +215,9 @@ __global__ void __launch_bounds__(256) xent_vec_kernel(
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int j = 4 * c + e;
-            double sm = (double)v[u][k][e] * inv_s;
-            if (j == lbl) sm -= 1.0;
-            o[e] = (on && j < C) ? (float)(sm / denom) : 0.f;
+            double sm = (double)v[u][k][e] * scale;
+            if (j == lbl) sm -= inv_d;
+            o[e] = (on && j < C) ? (float)sm : 0.f;
           }
           gr[c] = make_float4(o[0], o[1], o[2], o[3]);
         }

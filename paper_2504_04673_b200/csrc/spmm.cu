@@ -135,10 +135,16 @@ struct Vec<8> {
   }
 };
 
-template <int G, int CPL, bool F64, int V, int MB = Tune<CPL, V>::MINB>
+// TWO (fp32 accumulation, !F64): two-level fp32 sums -- a window of 32
+// entries, folded into a second fp32 accumulator.  Error <= (32 + len/32)
+// ulp of the row's sum of |terms| (<= 64 ulp = 3.8e-6 for a 1024-entry
+// item), inside the 1e-5 contract, with 8 fewer registers than fp64 folds.
+template <int G, int CPL, bool F64, int V, int MB = Tune<CPL, V>::MINB,
+          int EE = Tune<CPL, V>::E, bool TWO = false>
 __global__ void __launch_bounds__(256, MB)
     spmm_kernel(const __grid_constant__ SpmmArgs a) {
-  constexpr int E = Tune<CPL, V>::E;        // entries per pipeline step
+  constexpr int E = EE;                     // entries per pipeline step
+  static_assert(!(TWO && F64), "TWO is an fp32 mode");
   constexpr int E4 = E / 2;                 // int4 loads per step
   const int lig = threadIdx.x & (G - 1);
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -162,10 +168,17 @@ __global__ void __launch_bounds__(256, MB)
   }
   float part[CPL][V];
   double acc[F64 ? CPL : 1][V];
+  float acc2[TWO ? CPL : 1][V];
 #pragma unroll
   for (int q = 0; q < CPL; ++q)
 #pragma unroll
     for (int k = 0; k < V; ++k) part[q][k] = 0.f;
+  if constexpr (TWO) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int k = 0; k < V; ++k) acc2[q][k] = 0.f;
+  }
   if constexpr (F64) {
 #pragma unroll
     for (int q = 0; q < CPL; ++q)
@@ -225,7 +238,24 @@ __global__ void __launch_bounds__(256, MB)
           acc[q][k] += (double)part[q][k];
           part[q][k] = 0.f;
         }
+    } else if constexpr (TWO) {
+      constexpr int WS = 32 / E;            // steps per 32-entry window
+      if (s % WS == WS - 1) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q)
+#pragma unroll
+          for (int k = 0; k < V; ++k) {
+            acc2[q][k] += part[q][k];
+            part[q][k] = 0.f;
+          }
+      }
     }
+  }
+  if constexpr (TWO) {
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int k = 0; k < V; ++k) part[q][k] += acc2[q][k];
   }
 
   if (it.slot < 0) {
@@ -313,11 +343,12 @@ int bucket_of(int32_t len) {
   return (int)(4.0 * std::log2((double)len)) + 1;
 }
 
-template <int G, int CPL, bool F64, int V, int MB = Tune<CPL, V>::MINB>
+template <int G, int CPL, bool F64, int V, int MB = Tune<CPL, V>::MINB,
+          int EE = Tune<CPL, V>::E, bool TWO = false>
 void launch_spmm(const SpmmArgs& a, int nslabs, cudaStream_t s) {
   const int64_t threads = a.n_items * G;
   const unsigned gx = (unsigned)((threads + 255) / 256);
-  spmm_kernel<G, CPL, F64, V, MB><<<dim3(gx, nslabs), 256, 0, s>>>(a);
+  spmm_kernel<G, CPL, F64, V, MB, EE, TWO><<<dim3(gx, nslabs), 256, 0, s>>>(a);
 }
 
 using LaunchFn = void (*)(const SpmmArgs&, int, cudaStream_t);
@@ -349,6 +380,18 @@ LaunchFn pick_minb(int G, int MB) {
   if (G == g && MB == m) return &launch_spmm<g, 1, true, 8, m>;
   DG_CASE(2, 3) DG_CASE(4, 3) DG_CASE(8, 3) DG_CASE(16, 3) DG_CASE(32, 3)
   DG_CASE(2, 4) DG_CASE(4, 4) DG_CASE(8, 4) DG_CASE(16, 4) DG_CASE(32, 4)
+#undef DG_CASE
+  return nullptr;
+}
+
+// experiment grid (DG_SPMM_E / DG_SPMM_TWO): pipeline depth, accumulation
+LaunchFn pick_exp(int G, int MB, int E, bool two) {
+#define DG_CASE(g, m, e)                                                 \
+  if (G == g && MB == m && E == e)                                       \
+    return two ? &launch_spmm<g, 1, false, 8, m, e, true>                \
+               : &launch_spmm<g, 1, true, 8, m, e, false>;
+  DG_CASE(8, 3, 2) DG_CASE(8, 4, 2) DG_CASE(16, 3, 2) DG_CASE(16, 4, 2)
+  DG_CASE(8, 3, 4) DG_CASE(8, 4, 4) DG_CASE(16, 3, 4) DG_CASE(16, 4, 4)
 #undef DG_CASE
   return nullptr;
 }
@@ -699,6 +742,10 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   LaunchFn fn = v8 ? (acc ? pick_launch<true, 8>(G, CPL) : pick_launch<false, 8>(G, CPL))
                    : (acc ? pick_launch<true, 4>(G, CPL) : pick_launch<false, 4>(G, CPL));
   if (v8 && acc && CPL == 1 && minb >= 3) fn = pick_minb(G, minb);
+  static const int env_e = env_int("DG_SPMM_E", 0);
+  static const int env_two = env_int("DG_SPMM_TWO", 0);
+  if (v8 && acc && CPL == 1 && (env_e || env_two))
+    fn = pick_exp(G, minb ? minb : 3, env_e ? env_e : 4, env_two != 0);
   if (!fn) return set_err(DG_ERR_ARG, "dg_spmm_run: no kernel for config");
   fn(a, ns, S(stream));
   DG_LAUNCHED();

@@ -232,7 +232,12 @@ class _Dense:
 
     @staticmethod
     def _rows_ok(K, N):
-        return N <= 64 and K * 16 * ((N + 15) // 16) <= 16384
+        """dg_dense_rows' range: output rows <= 256 floats, B (K x N, padded)
+        in shared memory."""
+        ld = pad4(N)
+        nt = 4 if ld <= 4 else (8 if ld <= 8 else 16)
+        nc = -(-ld // nt)
+        return nc <= 16 and (((K + 3) // 4 * 4) * nc * nt + (256 // nc) * 36) * 4 <= 200 * 1024
 
     def fwd(self, t, w, f_in, f_out, relu):
         """z = t @ w (padded), h = relu(z) if requested (gcn.py:274-276)."""
@@ -264,7 +269,8 @@ class _Dense:
     def wgrad(self, h, m, f_in, f_out, ld_in, ld_out):
         """y = h^T m as an (ld_in x ld_out) zero-padded matrix (gcn.py:280)."""
         n = h.shape[0]
-        if f_out > 64 or ld_out > 16 * ((f_out + 15) // 16):
+        npt = 16 * ((f_out + 15) // 16) if f_out <= 64 else 64 * ((f_out + 63) // 64)
+        if f_out > 256 or ld_out > npt:
             return torch.mm(h.T, m)
         lib = L.lib()
         need = int(lib.dg_dense_tn_work(n, ld_in, f_out))

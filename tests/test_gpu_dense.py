@@ -20,10 +20,13 @@ def _pad(x, ld):
 
 
 @pytest.mark.parametrize("n,fi,fo", [(1000, 602, 16), (777, 16, 41), (5000, 100, 16),
-                                     (333, 16, 47), (64, 3, 2), (1, 16, 16)])
+                                     (333, 16, 47), (64, 3, 2), (1, 16, 16), (3001, 16, 172),
+                                     (1500, 128, 16), (700, 16, 250), (257, 41, 7)])
 def test_dense_fwd_bwd_wgrad(n, fi, fo):
     torch.manual_seed(n + fi + fo)
     d = _Dense(torch.device("cuda"))
+    assert d._rows_ok(fi, fo) and d._rows_ok(fo, fi)     # our kernels, not cuBLAS
+    l0 = L.launch_count()
     li, lo = pad4(fi), pad4(fo)
     t = _pad(torch.randn(n, fi, device="cuda"), li)
     w = torch.zeros((li, lo), device="cuda")
@@ -49,6 +52,7 @@ def test_dense_fwd_bwd_wgrad(n, fi, fo):
     assert not y[fi:, :].any() and not y[:, fo:].any()
     y2 = d.wgrad(t, m, fi, fo, li, lo)
     assert torch.equal(y, y2)                      # deterministic
+    assert L.launch_count() - l0 == 2 + 2 * 2     # rows x2, tn + reduce x2
 
 
 @pytest.mark.parametrize("n,C", [(10, 4), (1000, 41), (4097, 47), (300, 16), (50, 172),
