@@ -1,16 +1,18 @@
 // dense.cu -- the GCN's dense transforms, tall-skinny and memory-bound:
 //
-//   forward   Z = T W            gcn.py:274  (T: n x K, W: K x N, N <= 256)
+//   forward   Z = T W            gcn.py:274  (T: n x K, W: K x N, N <= 64)
 //             H = relu(Z)        gcn.py:276  (fused epilogue, optional)
 //   backward  G = (M W^T) * 1[Zprev > 0]     gcn.py:282  (fused mask, optional)
-//   wgrad     Y = H^T M          gcn.py:280  (K x N, reduction over the n rows)
+//   wgrad     Y = H^T M          gcn.py:280  (K x N, N <= 256, reduction over the n rows)
 //
 // fp32 SIMT (TF32 would break the fp32 parity contract); these shapes are
 // HBM-bound (T or H is read once: 566 MB for Reddit layer 1), so the target
 // is streaming the tall operand at HBM speed, not tensor-core FLOPs.
 //
-// dg_dense_rows: thread = one row x 16 output columns, A staged through
-// shared memory once per chunk (see dense_rw_kernel); any N up to 256.
+// dg_dense_rows: a CTA owns 64 rows x all N columns; B lives in shared
+// memory (K x N <= 16K floats); A is staged in 32-wide k-chunks, transposed
+// so a thread reads 4 consecutive rows with one 16-B shared load; thread
+// tile 4 rows x N/16 columns.
 //
 // dg_dense_tn: grid = (row slices, 64-wide K blocks); each CTA accumulates
 // its slice's partial H^T M (fp32 per 64-row chunk, folded into fp64) and
@@ -21,50 +23,45 @@
 
 namespace {
 
-// Row-wise form (dg_dense_rows): thread = (one row, NT consecutive output
-// columns); a CTA covers RB = 256 / NC rows x all NC column chunks.  A is
-// staged through shared memory in KC-wide chunks with coalesced float4 loads
-// (the next chunk in flight in registers) and each thread reads its own
-// row's values once per chunk (one LDS.128 per 4 k); B (K x NP, zero padded)
-// sits in shared memory and is read as broadcast float4s.  Every A element
-// crosses shared memory twice (store + one read per column chunk), so the
-// kernel streams A at HBM speed instead of being shared-memory bound.
-constexpr int KC = 32;   // k-chunk of the row-wise kernel
+constexpr int BM = 64;   // rows per CTA (dense_rows)
+constexpr int BK = 32;   // k-chunk (2 float4 per thread in flight)
 
-template <int NT>
-__global__ void __launch_bounds__(256) dense_rw_kernel(
+template <int TN>
+__global__ void __launch_bounds__(256) dense_rows_kernel(
     const float* __restrict__ A, int64_t lda, int64_t n, int K, const float* __restrict__ B,
     int64_t ldb, int N, int transB, float* __restrict__ C, int64_t ldc,
-    float* __restrict__ Crelu, const float* __restrict__ Zmask, int64_t ldm, int NC) {
-  extern __shared__ __align__(16) float smem[];
-  const int RB = 256 / NC;                           // rows per CTA
-  const int NP = NC * NT;                            // padded output width
-  const int Kp = (K + 3) & ~3;
-  float* Bs = smem;                                  // Kp x NP
-  float* As = smem + (size_t)Kp * NP;                // RB x (KC + 4)
+    float* __restrict__ Crelu, const float* __restrict__ Zmask, int64_t ldm) {
+  extern __shared__ float smem[];
+  constexpr int NP = 16 * TN;                       // padded N
+  float* Bs = smem;                                  // K x NP
+  float* As = smem + (size_t)K * NP;                 // BK x (BM + 4)
   const int tid = threadIdx.x;
-  for (int i = tid; i < Kp * NP; i += 256) {
+  const int tx = tid % 16;                           // column group
+  const int ty = tid / 16;                           // row group (4 rows)
+  for (int i = tid; i < K * NP; i += 256) {
     const int k = i / NP, j = i % NP;
     float b = 0.f;
-    if (k < K && j < N) b = transB ? B[(int64_t)j * ldb + k] : B[(int64_t)k * ldb + j];
+    if (j < N) b = transB ? B[(int64_t)j * ldb + k] : B[(int64_t)k * ldb + j];
     Bs[i] = b;
   }
-  const int r = tid / NC, c = tid % NC;
-  const int64_t row0 = (int64_t)blockIdx.x * RB;
-  const int per = (RB * (KC / 4) + 255) / 256;       // float4 per thread per chunk (<= 8)
-  float acc[NT];
+  const int64_t row0 = (int64_t)blockIdx.x * BM;
+  float acc[4][TN];
 #pragma unroll
-  for (int j = 0; j < NT; ++j) acc[j] = 0.f;
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < TN; ++c) acc[r][c] = 0.f;
+  // A chunk loader: each thread owns 2 float4 of the 64 x 32 chunk; the
+  // next chunk is loaded into registers while the current one is consumed
+  constexpr int PER = BM * BK / 4 / 256;            // float4 per thread (2)
   auto load_chunk = [&](int k0, float4* v) {
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (u >= per) continue;
+    for (int u = 0; u < PER; ++u) {
       const int i = tid + u * 256;
-      const int rr = i / (KC / 4), q = i % (KC / 4);
-      const int64_t gr = row0 + rr;
+      const int r = i / (BK / 4), q = i % (BK / 4);
+      const int64_t gr = row0 + r;
       const int k = k0 + 4 * q;
-      if (rr < RB && gr < n && k < K) {
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gr < n && k < K) {
         const float* ap = A + gr * lda + k;
         if (k + 3 < K) {
           v[u] = __ldcs(reinterpret_cast<const float4*>(ap));
@@ -76,57 +73,51 @@ __global__ void __launch_bounds__(256) dense_rw_kernel(
       }
     }
   };
-  float4 nxt[8];
+  float4 nxt[PER];
   load_chunk(0, nxt);
-  const float* arow = As + (size_t)r * (KC + 4);
-  for (int k0 = 0; k0 < K; k0 += KC) {
+  for (int k0 = 0; k0 < K; k0 += BK) {
     __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      if (u >= per) continue;
+    for (int u = 0; u < PER; ++u) {                  // stage transposed: As[k][r]
       const int i = tid + u * 256;
-      const int rr = i / (KC / 4), q = i % (KC / 4);
-      if (rr < RB) *reinterpret_cast<float4*>(&As[(size_t)rr * (KC + 4) + 4 * q]) = nxt[u];
+      const int r = i / (BK / 4), q = i % (BK / 4);
+      As[(4 * q + 0) * (BM + 4) + r] = nxt[u].x;
+      As[(4 * q + 1) * (BM + 4) + r] = nxt[u].y;
+      As[(4 * q + 2) * (BM + 4) + r] = nxt[u].z;
+      As[(4 * q + 3) * (BM + 4) + r] = nxt[u].w;
     }
     __syncthreads();
-    if (k0 + KC < K) load_chunk(k0 + KC, nxt);       // in flight during the math
-    const int kmax = min(KC, Kp - k0);
-    if (r < RB) {
-      for (int kk = 0; kk < kmax; kk += 4) {
-        const float4 a = *reinterpret_cast<const float4*>(arow + kk);
-        const float av[4] = {a.x, a.y, a.z, a.w};
+    if (k0 + BK < K) load_chunk(k0 + BK, nxt);       // in flight during the math
+    const int kmax = min(BK, K - k0);
+#pragma unroll 8
+    for (int kk = 0; kk < kmax; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[kk * (BM + 4) + 4 * ty]);
+      const float* bp = &Bs[(k0 + kk) * NP + tx * TN];
+      float b[TN];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float4* bp = reinterpret_cast<const float4*>(Bs + (size_t)(k0 + kk + e) * NP +
-                                                             c * NT);
+      for (int c = 0; c < TN; ++c) b[c] = bp[c];
 #pragma unroll
-          for (int j4 = 0; j4 < NT / 4; ++j4) {
-            const float4 b = bp[j4];
-            acc[4 * j4 + 0] = fmaf(av[e], b.x, acc[4 * j4 + 0]);
-            acc[4 * j4 + 1] = fmaf(av[e], b.y, acc[4 * j4 + 1]);
-            acc[4 * j4 + 2] = fmaf(av[e], b.z, acc[4 * j4 + 2]);
-            acc[4 * j4 + 3] = fmaf(av[e], b.w, acc[4 * j4 + 3]);
-          }
-        }
+      for (int c = 0; c < TN; ++c) {
+        acc[0][c] = fmaf(a.x, b[c], acc[0][c]);
+        acc[1][c] = fmaf(a.y, b[c], acc[1][c]);
+        acc[2][c] = fmaf(a.z, b[c], acc[2][c]);
+        acc[3][c] = fmaf(a.w, b[c], acc[3][c]);
       }
     }
   }
-  const int64_t gr = row0 + r;
-  if (r >= RB || gr >= n) return;
 #pragma unroll
-  for (int j4 = 0; j4 < NT / 4; ++j4) {
-    const int j = c * NT + 4 * j4;
-    if (j >= ldc) break;
-    float o[4] = {acc[4 * j4], acc[4 * j4 + 1], acc[4 * j4 + 2], acc[4 * j4 + 3]};
-    if (Zmask) {
+  for (int r = 0; r < 4; ++r) {
+    const int64_t gr = row0 + 4 * ty + r;
+    if (gr >= n) continue;
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        if (j + e < N && !(Zmask[gr * ldm + j + e] > 0.f)) o[e] = 0.f;
+    for (int c = 0; c < TN; ++c) {
+      const int j = tx * TN + c;
+      if (j >= ldc) continue;
+      float v = acc[r][c];
+      if (Zmask && j < N && !(Zmask[gr * ldm + j] > 0.f)) v = 0.f;
+      C[gr * ldc + j] = v;
+      if (Crelu) Crelu[gr * ldc + j] = fmaxf(v, 0.f);
     }
-    *reinterpret_cast<float4*>(C + gr * ldc + j) = make_float4(o[0], o[1], o[2], o[3]);
-    if (Crelu)
-      *reinterpret_cast<float4*>(Crelu + gr * ldc + j) =
-          make_float4(fmaxf(o[0], 0.f), fmaxf(o[1], 0.f), fmaxf(o[2], 0.f), fmaxf(o[3], 0.f));
   }
 }
 
@@ -259,34 +250,30 @@ extern "C" {
 int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float* B, int64_t ldb,
                   int32_t N, int32_t transB, float* C, int64_t ldc, float* C_relu,
                   const float* z_mask, int64_t ld_mask, void* stream) {
-  // NT output columns per thread: 16 (4 float4) unless the row is narrower
-  const int NT = ldc <= 4 ? 4 : (ldc <= 8 ? 8 : 16);
-  const int NC = (int)((ldc + NT - 1) / NT);
-  const int Kp = (K + 3) & ~3;
-  if (n < 0 || K < 1 || N < 1 || N > ldc || (ldc & 3) || NC > 16 || (lda & 3) ||
-      ((uintptr_t)A & 15) || ((uintptr_t)C & 15) || (C_relu && ((uintptr_t)C_relu & 15)))
+  const int TN = tn_of(N);
+  if (n < 0 || K < 1 || N < 1 || N > 64 || (int64_t)K * 16 * TN > 16384 || (lda & 3) ||
+      ((uintptr_t)A & 15))
     return set_err(DG_ERR_ARG, "dense_rows: shape outside the kernel's range");
-  const int RB = 256 / NC;
-  const size_t smem = ((size_t)Kp * NC * NT + (size_t)RB * (KC + 4)) * sizeof(float);
-  if (smem > 200 * 1024) return set_err(DG_ERR_ARG, "dense_rows: B too large for shared memory");
   if (n == 0) return DG_OK;
-  const unsigned blocks = (unsigned)((n + RB - 1) / RB);
+  const size_t smem = ((size_t)K * 16 * TN + (size_t)BK * (BM + 4)) * sizeof(float);
+  const unsigned blocks = (unsigned)((n + BM - 1) / BM);
   cudaStream_t st = S(stream);
-#define DG_DR(nt)                                                                           \
-  do {                                                                                      \
-    static bool attr = false;                                                               \
-    if (!attr) {                                                                            \
-      DG_CK(cudaFuncSetAttribute(dense_rw_kernel<nt>,                                       \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)); \
-      attr = true;                                                                          \
-    }                                                                                       \
-    dense_rw_kernel<nt><<<blocks, 256, smem, st>>>(A, lda, n, K, B, ldb, N, transB, C, ldc, \
-                                                   C_relu, z_mask, ld_mask, NC);            \
+#define DG_DR(tn)                                                                          \
+  do {                                                                                     \
+    static bool attr = false;                                                              \
+    if (!attr) {                                                                           \
+      DG_CK(cudaFuncSetAttribute(dense_rows_kernel<tn>,                                    \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)); \
+      attr = true;                                                                         \
+    }                                                                                      \
+    dense_rows_kernel<tn><<<blocks, 256, smem, st>>>(A, lda, n, K, B, ldb, N, transB, C, ldc, \
+                                                     C_relu, z_mask, ld_mask);             \
   } while (0)
-  switch (NT) {
-    case 4: DG_DR(4); break;
-    case 8: DG_DR(8); break;
-    default: DG_DR(16); break;
+  switch (TN) {
+    case 1: DG_DR(1); break;
+    case 2: DG_DR(2); break;
+    case 3: DG_DR(3); break;
+    default: DG_DR(4); break;
   }
 #undef DG_DR
   DG_LAUNCHED();

@@ -232,12 +232,7 @@ class _Dense:
 
     @staticmethod
     def _rows_ok(K, N):
-        """dg_dense_rows' range: output rows <= 256 floats, B (K x N, padded)
-        in shared memory."""
-        ld = pad4(N)
-        nt = 4 if ld <= 4 else (8 if ld <= 8 else 16)
-        nc = -(-ld // nt)
-        return nc <= 16 and (((K + 3) // 4 * 4) * nc * nt + (256 // nc) * 36) * 4 <= 200 * 1024
+        return N <= 64 and K * 16 * ((N + 15) // 16) <= 16384
 
     def fwd(self, t, w, f_in, f_out, relu):
         """z = t @ w (padded), h = relu(z) if requested (gcn.py:274-276)."""
