@@ -111,12 +111,6 @@ int dg_group_reduce(int g, const float* const* src, int n_dst, float* const* dst
  *      each process writes `epoch` to slot `me` of every peer and waits for
  *      all slots of its own array to reach `epoch`.  Bounded by timeout_ns;
  *      on timeout sets *err_dev = 1 instead of hanging the GPU.          */
-/* Pairwise form (pipelined exchange): dg_signal stores `value` into a peer's
- * flag slot (system-scope release, after a system fence); dg_wait spins on a
- * local slot until it reaches `value` (acquire), bounded by timeout_ns.    */
-int dg_signal(uint64_t* remote_slot, uint64_t value, void* stream);
-int dg_wait(const uint64_t* local_slot, uint64_t value, int64_t timeout_ns, int32_t* err_dev,
-            void* stream);
 int dg_barrier(uint64_t* const* flags, int n_procs, int me, uint64_t epoch,
                int64_t timeout_ns, int32_t* err_dev, void* stream);
 

@@ -55,8 +55,6 @@ _SIGS = {
     "dg_group_reduce": (C.c_int, [C.c_int, c_vpp, C.c_int, c_vpp, C.c_int64, C.c_int64,
                                   C.c_int32, c_vp]),
     "dg_barrier": (C.c_int, [c_vpp, C.c_int, C.c_int, C.c_uint64, C.c_int64, c_vp, c_vp]),
-    "dg_signal": (C.c_int, [c_vp, C.c_uint64, c_vp]),
-    "dg_wait": (C.c_int, [c_vp, C.c_uint64, C.c_int64, c_vp, c_vp]),
     "dg_xent": (C.c_int, [c_vp, C.c_int64, C.c_int32, C.c_int64, c_vp, c_vp, C.c_double, c_vp,
                           C.c_int64, c_vp, c_vp, c_vp, c_vp]),
     "dg_relu": (C.c_int, [c_vp, c_vp, C.c_int64, C.c_int32, C.c_int64, c_vp]),

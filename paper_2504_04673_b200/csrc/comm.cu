@@ -268,46 +268,9 @@ __global__ void barrier_kernel(const __grid_constant__ BArgs a) {
   __syncthreads();
 }
 
-// Pairwise signal / wait (pipelined exchange): the sender, after its peer
-// stores to one destination process, publishes `value` into that process's
-// flag slot; the receiver's stream spins until its slot reaches `value`
-// before the SpMM pass over those halo rows.
-__global__ void signal_kernel(uint64_t* remote, uint64_t v) {
-  __threadfence_system();
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(remote), "l"(v) : "memory");
-}
-
-__global__ void wait_kernel(const uint64_t* mine, uint64_t v, int64_t timeout_ns, int32_t* err) {
-  const uint64_t t0 = gtimer();
-  while (true) {
-    uint64_t x;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(x) : "l"(mine) : "memory");
-    if (x >= v) break;
-    if (gtimer() - t0 > (uint64_t)timeout_ns) {
-      atomicExch(err, 1);
-      break;
-    }
-  }
-}
-
 }  // namespace
 
 extern "C" {
-
-int dg_signal(uint64_t* remote_slot, uint64_t value, void* stream) {
-  if (!remote_slot) return set_err(DG_ERR_ARG, "signal: null slot");
-  signal_kernel<<<1, 1, 0, S(stream)>>>(remote_slot, value);
-  DG_LAUNCHED();
-  return DG_OK;
-}
-
-int dg_wait(const uint64_t* local_slot, uint64_t value, int64_t timeout_ns, int32_t* err_dev,
-            void* stream) {
-  if (!local_slot || !err_dev) return set_err(DG_ERR_ARG, "wait: null slot");
-  wait_kernel<<<1, 1, 0, S(stream)>>>(local_slot, value, timeout_ns, err_dev);
-  DG_LAUNCHED();
-  return DG_OK;
-}
 
 int dg_group_reduce(int g, const float* const* src, int n_dst, float* const* dst, int64_t lo,
                     int64_t hi, int32_t fence_sys, void* stream) {

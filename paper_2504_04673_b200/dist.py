@@ -69,8 +69,6 @@ class World:
                 except L.DgError:
                     pass
         self._flags = SymBuffer(self, 8 * self.size)
-        self._sig = SymBuffer(self, 8 * self.size)       # pairwise signal slots
-        self._sig_round = 0
         self._err = torch.zeros(1, dtype=torch.int32, device=self.device)
         return self
 
@@ -95,23 +93,6 @@ class World:
         ptrs = (C.c_void_p * self.size)(*self._flags.ptrs)
         L.check(L.lib().dg_barrier(ptrs, self.size, self.proc, self._epoch, BARRIER_TIMEOUT_NS,
                                    self._err.data_ptr(), L.stream_ptr()))
-
-    def next_round(self):
-        """Advance the pairwise-signal round (once per pipelined phase, in
-        lockstep on every process); returns the round's value."""
-        self._sig_round += 1
-        return self._sig_round
-
-    def signal(self, peer, value):
-        """Publish `value` into process `peer`'s slot for this process (after
-        this stream's prior peer stores), on the current stream."""
-        L.check(L.lib().dg_signal(C.c_void_p(self._sig.ptrs[peer] + 8 * self.proc),
-                                  C.c_uint64(value), L.stream_ptr()))
-
-    def wait_from(self, peer, value):
-        """Stall the current stream until process `peer` has signalled `value`."""
-        L.check(L.lib().dg_wait(C.c_void_p(self._sig.local + 8 * peer), C.c_uint64(value),
-                                BARRIER_TIMEOUT_NS, self._err.data_ptr(), L.stream_ptr()))
 
     def check(self):
         """Raise if a device barrier timed out (call at sync points)."""

@@ -134,14 +134,11 @@ def _check_bounds(vplan, local):
 
 
 class _Part:
-    """A rank operand restricted to the entries whose extended column lies
-    in [lo, hi) -- the own block (interior), all halo rows (boundary), or
-    the halo rows received from one process -- storage order kept."""
+    """A rank operand restricted to its own-block (interior) or halo
+    (boundary) entries, storage order kept."""
 
-    def __init__(self, ro, lo, hi=None):
-        keep = ro.col_ext >= lo
-        if hi is not None:
-            keep &= ro.col_ext < hi
+    def __init__(self, ro, boundary):
+        keep = (ro.col_ext >= ro.n_local) if boundary else (ro.col_ext < ro.n_local)
         self.n_rows, self.n_local = ro.n_rows, ro.n_local
         self.row_ptr = np.zeros(ro.n_rows + 1, dtype=np.int64)
         if isinstance(ro.col_ext, torch.Tensor):       # operand resident in HBM
@@ -196,48 +193,33 @@ class DevicePlan:
         ro = [vplan.ranks[r] for r in self.local]
         _check_bounds(vplan, self.local)
         self.overlap = self.multi
-        w, p = self.world, vplan.grid.p
-        self._hplans, self._xplans = {}, {}
         if self.overlap:
-            self._splan = _make_spmm_plan([_Part(x, 0, x.n_local) for x in ro], max_chunk)
-            # Pipelined halo: the halo entries are grouped by the process their
-            # rows come from, in arrival order d = (me - source) mod N, so the
-            # SpMM over one source's rows runs while the next source's rows
-            # are still arriving (pairwise signals, no all-process barrier).
-            ranges = {r: {} for r in self.local}
-            for sg in vplan.segments:
-                if sg.dst in ranges and sg.count > 0:
-                    d = (w.proc - w.proc_of(sg.src, p)) % w.size
-                    lo, hi = ranges[sg.dst].get(d, (None, None))
-                    a, b = sg.dst_row0, sg.dst_row0 + sg.count
-                    ranges[sg.dst][d] = (a if lo is None else min(lo, a),
-                                         b if hi is None else max(hi, b))
-            for d in range(w.size):
-                parts = []
-                for x, r in zip(ro, self.local):
-                    lo, hi = ranges[r].get(d, (0, 0))
-                    parts.append(_Part(x, x.n_local + lo, x.n_local + hi))
-                if any(_numel(pt.col_ext) for pt in parts):
-                    self._hplans[d] = _make_spmm_plan(parts, max_chunk,
-                                                      L.DG_PLAN_SKIP_EMPTY_ROWS)
+            self._splan = _make_spmm_plan([_Part(x, False) for x in ro], max_chunk)
+            self._bplan = _make_spmm_plan([_Part(x, True) for x in ro], max_chunk,
+                                          L.DG_PLAN_SKIP_EMPTY_ROWS)
             # high priority: the exchange's blocks are dispatched ahead of the
             # own-block SpMM's (otherwise the 10^5-block SpMM grid starves it)
             self._side = torch.cuda.Stream(device=self.device, priority=-1)
         else:
             self._splan = _make_spmm_plan(ro, max_chunk)
+            self._bplan = None
         segs = [s for s in vplan.segments if s.src in self.li and s.count > 0]
         # blocks are dispatched roughly in segment order: rotate every
         # sender's destinations by process distance so that at any moment
         # each GPU receives from one sender (no incast on one NVLink ingress)
-        dist = lambda sg: (w.proc_of(sg.dst, p) - w.proc_of(sg.src, p)) % w.size  # noqa: E731
-        segs.sort(key=lambda sg: (dist(sg), (sg.dst - sg.src) % p, sg.src))
+        w, p = self.world, vplan.grid.p
+        segs.sort(key=lambda sg: ((w.proc_of(sg.dst, p) - w.proc_of(sg.src, p)) % w.size,
+                                  (sg.dst - sg.src) % p, sg.src))
         self._segs = segs
-        self._xplan = self._xchg_plan(segs)
-        if self.overlap:
-            for d in range(w.size):
-                grp = [sg for sg in segs if dist(sg) == d]
-                if grp:
-                    self._xplans[d] = self._xchg_plan(grp)
+        xh = C.c_void_p()
+        L.check(lib.dg_xchg_plan_create(
+            C.byref(xh), len(segs), L.i32_array([self.li[s.src] for s in segs]),
+            L.i64_array([s.count for s in segs]),
+            (C.c_void_p * max(len(segs), 1))(*[0 if s.idx is None else _ptr(s.idx)
+                                               for s in segs]),
+            L.i64_array([0] * len(segs)), L.i32_array([s.dst for s in segs]),
+            L.i64_array([s.dst_row0 for s in segs])))
+        self._xplan = xh
         self.one_d = vplan.variant.startswith("1d")
         self.reduce = (not self.one_d) and self.grid.c > 1
         self.halo = {r: None for r in self.local}
@@ -259,17 +241,6 @@ class DevicePlan:
                 x.col_ext = x.val = None
         if self.multi:
             self._init_symmetric(max_ld)
-
-    def _xchg_plan(self, segs):
-        xh = C.c_void_p()
-        L.check(L.lib().dg_xchg_plan_create(
-            C.byref(xh), len(segs), L.i32_array([self.li[s.src] for s in segs]),
-            L.i64_array([s.count for s in segs]),
-            (C.c_void_p * max(len(segs), 1))(*[0 if s.idx is None else _ptr(s.idx)
-                                               for s in segs]),
-            L.i64_array([0] * len(segs)), L.i32_array([s.dst for s in segs]),
-            L.i64_array([s.dst_row0 for s in segs])))
-        return xh
 
     # ---- multi-process symmetric buffers --------------------------------
     def _init_symmetric(self, max_ld):
@@ -314,16 +285,11 @@ class DevicePlan:
 
     def _destroy_plans(self):
         lib = L.lib()
-        for name in ("_splan", "_xplan"):
+        for name in ("_splan", "_bplan", "_xplan"):
             h = getattr(self, name, None)
             if h:
                 (lib.dg_xchg_plan_destroy if name == "_xplan" else lib.dg_spmm_plan_destroy)(h)
                 setattr(self, name, None)
-        for h in getattr(self, "_hplans", {}).values():
-            lib.dg_spmm_plan_destroy(h)
-        for h in getattr(self, "_xplans", {}).values():
-            lib.dg_xchg_plan_destroy(h)
-        self._hplans, self._xplans = {}, {}
 
     def __del__(self):
         try:
@@ -344,10 +310,9 @@ class DevicePlan:
                                     L.ptr_array(halo_ptrs), L.ptr_array(zp), f, ld, ld, self.acc,
                                     0, beta, stream))
 
-    def _xchg(self, hs, dst, f, ld, stream, plan=None):
+    def _xchg(self, hs, dst, f, ld, stream):
         if self._segs:
-            L.check(L.lib().dg_xchg_run(plan or self._xplan,
-                                        L.ptr_array([hs[r] for r in self.local]),
+            L.check(L.lib().dg_xchg_run(self._xplan, L.ptr_array([hs[r] for r in self.local]),
                                         len(self.local), L.ptr_array(dst), len(dst), f, ld,
                                         1 if self.multi else 0, stream))
 
@@ -400,35 +365,19 @@ class DevicePlan:
         dst = [self._halo_ptr(d, par) for d in range(p)]
         halo_ptrs = [self._halo_ptr(r, par) for r in self.local]
         main = torch.cuda.current_stream()
-        w = self.world
-        rnd = w.next_round()
         self._side.wait_stream(main)                    # H is ready
         with torch.cuda.stream(self._side):
-            sp = L.stream_ptr(self._side)
             if self.parities == 1:
                 # every peer has finished reading its (single) halo buffer
                 # in the previous phase before anyone overwrites it
-                w.barrier()
-            for d in range(w.size):                     # destination = me + d
-                if d in self._xplans:
-                    self._xchg(hs, dst, f, ld, sp, self._xplans[d])
-                if d == 0:
-                    local_done = torch.cuda.Event()
-                    local_done.record(self._side)
-                else:
-                    # every pair signals every phase, empty or not: the chain
-                    # of waits is what makes the double-buffered halos safe
-                    w.signal((w.proc + d) % w.size, rnd)
+                self.world.barrier()
+            self._xchg(hs, dst, f, ld, L.stream_ptr(self._side))
+            self.world.barrier()                        # every peer's rows have landed
         zp = ([self._partial_ptr(r, par) for r in self.local] if self.reduce
               else [out[r].data_ptr() for r in self.local])
         self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, st)       # own block
-        for d in range(w.size):                         # source = me - d, arrival order
-            if d == 0:
-                main.wait_event(local_done)
-            else:
-                w.wait_from((w.proc - d) % w.size, rnd)
-            if d in self._hplans:
-                self._spmm(self._hplans[d], hs, halo_ptrs, zp, f, ld, 1, st)   # z +=
+        main.wait_stream(self._side)
+        self._spmm(self._bplan, hs, halo_ptrs, zp, f, ld, 1, st)       # halo rows, z +=
         for r in self.local:                            # inputs in use on the side stream
             hs[r].record_stream(self._side)
         if self.reduce and not reduce:
@@ -474,8 +423,8 @@ class DevicePlan:
                                       ld).data_ptr() for r in self.local]
         zp = [out[r].data_ptr() for r in self.local]
         self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, _stream())
-        for d in sorted(self._hplans):
-            self._spmm(self._hplans[d], hs, halo_ptrs, zp, f, ld, 1, _stream())
+        if self._bplan is not None:
+            self._spmm(self._bplan, hs, halo_ptrs, zp, f, ld, 1, _stream())
 
     def traffic_rows(self):
         """(rows sent, rows received) per rank in one phase."""
