@@ -264,8 +264,8 @@ class _Dense:
     def wgrad(self, h, m, f_in, f_out, ld_in, ld_out):
         """y = h^T m as an (ld_in x ld_out) zero-padded matrix (gcn.py:280)."""
         n = h.shape[0]
-        npt = 16 * ((f_out + 15) // 16) if f_out <= 64 else 64 * ((f_out + 63) // 64)
-        if f_out > 256 or ld_out > npt:
+        # N > 64 (papers-shaped C=172): cuBLAS measured faster (12.6 vs 21 ms)
+        if f_out > 64 or ld_out > 16 * ((f_out + 15) // 16):
             return torch.mm(h.T, m)
         lib = L.lib()
         need = int(lib.dg_dense_tn_work(n, ld_in, f_out))
