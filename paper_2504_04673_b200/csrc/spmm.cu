@@ -139,12 +139,18 @@ struct Vec<8> {
 // entries, folded into a second fp32 accumulator.  Error <= (32 + len/32)
 // ulp of the row's sum of |terms| (<= 64 ulp = 3.8e-6 for a 1024-entry
 // item), inside the 1e-5 contract, with 8 fewer registers than fp64 folds.
+// STG (experiment): the item's entries are staged into shared memory by
+// cp.async one 2G-entry window ahead (no registers held by the CSR
+// prefetch); every lane reads the window's (col, val) pairs as broadcasts.
 template <int G, int CPL, bool F64, int V, int MB = Tune<CPL, V>::MINB,
-          int EE = Tune<CPL, V>::E, bool TWO = false>
+          int EE = Tune<CPL, V>::E, bool TWO = false, bool STG = false>
 __global__ void __launch_bounds__(256, MB)
     spmm_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int E = EE;                     // entries per pipeline step
   static_assert(!(TWO && F64), "TWO is an fp32 mode");
+  constexpr int WIN = 2 * G;                // STG: entries per staged window (16 B per lane)
+  static_assert(!STG || (WIN % E == 0), "STG: window must hold whole steps");
+  __shared__ __align__(16) int2 stg[STG ? 256 / G : 1][2][STG ? WIN : 1];
   constexpr int E4 = E / 2;                 // int4 loads per step
   const int lig = threadIdx.x & (G - 1);
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -187,69 +193,154 @@ __global__ void __launch_bounds__(256, MB)
   }
 
   const int len = it.len;
-  const int n4 = (len + 1) >> 1;            // int4 words of this item
-  const int steps = (len + E - 1) / E;
-  int4 nx[E4];
-#pragma unroll
-  for (int u = 0; u < E4; ++u) nx[u] = (u < n4) ? ld_stream(ep + u, pol) : make_int4(0, 0, 0, 0);
+  if constexpr (!STG) {
+    const int n4 = (len + 1) >> 1;            // int4 words of this item
+    const int steps = (len + E - 1) / E;
+    int4 nx[E4];
+  #pragma unroll
+    for (int u = 0; u < E4; ++u) nx[u] = (u < n4) ? ld_stream(ep + u, pol) : make_int4(0, 0, 0, 0);
 
-  for (int s = 0; s < steps; ++s) {
-    int4 cur[E4];
-#pragma unroll
-    for (int u = 0; u < E4; ++u) cur[u] = nx[u];
-    if (s + 1 < steps) {                    // prefetch the next step's entries
-#pragma unroll
-      for (int u = 0; u < E4; ++u) {
-        const int w = (s + 1) * E4 + u;
-        nx[u] = (w < n4) ? ld_stream(ep + w, pol) : make_int4(0, 0, 0, 0);
-      }
-    }
-    const int nv = min(E, len - s * E);
-    Vec<V> x[E][CPL];
-    float v[E];
-#pragma unroll
-    for (int j = 0; j < E; ++j) {
-      const int c = (j & 1) ? cur[j >> 1].z : cur[j >> 1].x;
-      v[j] = __int_as_float((j & 1) ? cur[j >> 1].w : cur[j >> 1].y);
-      if (j < nv) {
-        const float* hp = c < nl ? hl + (int64_t)c * ld : hh + (int64_t)(c - nl) * ld;
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          if (on[q]) x[j][q].load(hp + (int64_t)chk[q] * V);
-          else x[j][q].zero();
+    for (int s = 0; s < steps; ++s) {
+      int4 cur[E4];
+  #pragma unroll
+      for (int u = 0; u < E4; ++u) cur[u] = nx[u];
+      if (s + 1 < steps) {                    // prefetch the next step's entries
+  #pragma unroll
+        for (int u = 0; u < E4; ++u) {
+          const int w = (s + 1) * E4 + u;
+          nx[u] = (w < n4) ? ld_stream(ep + w, pol) : make_int4(0, 0, 0, 0);
         }
-      } else {
-        v[j] = 0.f;
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) x[j][q].zero();
       }
-    }
-#pragma unroll
-    for (int j = 0; j < E; ++j)
-#pragma unroll
-      for (int q = 0; q < CPL; ++q)
-#pragma unroll
-        for (int k = 0; k < V; ++k) part[q][k] = fmaf(v[j], x[j][q].v[k], part[q][k]);
-    if constexpr (F64) {
-#pragma unroll
-      for (int q = 0; q < CPL; ++q)
-#pragma unroll
-        for (int k = 0; k < V; ++k) {
-          acc[q][k] += (double)part[q][k];
-          part[q][k] = 0.f;
+      const int nv = min(E, len - s * E);
+      Vec<V> x[E][CPL];
+      float v[E];
+  #pragma unroll
+      for (int j = 0; j < E; ++j) {
+        const int c = (j & 1) ? cur[j >> 1].z : cur[j >> 1].x;
+        v[j] = __int_as_float((j & 1) ? cur[j >> 1].w : cur[j >> 1].y);
+        if (j < nv) {
+          const float* hp = c < nl ? hl + (int64_t)c * ld : hh + (int64_t)(c - nl) * ld;
+  #pragma unroll
+          for (int q = 0; q < CPL; ++q) {
+            if (on[q]) x[j][q].load(hp + (int64_t)chk[q] * V);
+            else x[j][q].zero();
+          }
+        } else {
+          v[j] = 0.f;
+  #pragma unroll
+          for (int q = 0; q < CPL; ++q) x[j][q].zero();
         }
-    } else if constexpr (TWO) {
-      constexpr int WS = 32 / E;            // steps per 32-entry window
-      if (s % WS == WS - 1) {
-#pragma unroll
+      }
+  #pragma unroll
+      for (int j = 0; j < E; ++j)
+  #pragma unroll
         for (int q = 0; q < CPL; ++q)
-#pragma unroll
+  #pragma unroll
+          for (int k = 0; k < V; ++k) part[q][k] = fmaf(v[j], x[j][q].v[k], part[q][k]);
+      if constexpr (F64) {
+  #pragma unroll
+        for (int q = 0; q < CPL; ++q)
+  #pragma unroll
           for (int k = 0; k < V; ++k) {
-            acc2[q][k] += part[q][k];
+            acc[q][k] += (double)part[q][k];
             part[q][k] = 0.f;
           }
+      } else if constexpr (TWO) {
+        constexpr int WS = 32 / E;            // steps per 32-entry window
+        if (s % WS == WS - 1) {
+  #pragma unroll
+          for (int q = 0; q < CPL; ++q)
+  #pragma unroll
+            for (int k = 0; k < V; ++k) {
+              acc2[q][k] += part[q][k];
+              part[q][k] = 0.f;
+            }
+        }
       }
     }
+  } else {
+    // ---- staged entries: window w of the item lives in stg[grp][w & 1]
+    const int grp = (threadIdx.x & 255) / G;
+    const unsigned gmask = G == 32 ? 0xffffffffu
+                                   : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+    const int2* __restrict__ src = reinterpret_cast<const int2*>(R.ent) + it.lo;
+    const int nwin = (len + WIN - 1) / WIN;
+    const int len2 = (len + 1) & ~1;        // storage is padded to even entries
+    auto issue = [&](int w) {
+      const int e0 = w * WIN + 2 * lig;
+      int2* dst = &stg[grp][w & 1][2 * lig];
+      if (w < nwin && e0 < len2) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + e0)
+                     : "memory");
+      } else {
+        *reinterpret_cast<int4*>(dst) = make_int4(0, 0, 0, 0);
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    issue(0);
+    issue(1);
+    for (int w = 0; w < nwin; ++w) {
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncwarp(gmask);
+      const int2* win = stg[grp][w & 1];
+#pragma unroll
+      for (int st = 0; st < WIN / E; ++st) {
+        const int base = w * WIN + st * E;
+        if (base >= len) break;
+        const int nv = min(E, len - base);
+        Vec<V> x[E][CPL];
+        float v[E];
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const int2 en = win[st * E + j];
+          v[j] = __int_as_float(en.y);
+          if (j < nv) {
+            const int c = en.x;
+            const float* hp = c < nl ? hl + (int64_t)c * ld : hh + (int64_t)(c - nl) * ld;
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) {
+              if (on[q]) x[j][q].load(hp + (int64_t)chk[q] * V);
+              else x[j][q].zero();
+            }
+          } else {
+            v[j] = 0.f;
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) x[j][q].zero();
+          }
+        }
+        const int s = base / E;
+    #pragma unroll
+        for (int j = 0; j < E; ++j)
+    #pragma unroll
+          for (int q = 0; q < CPL; ++q)
+    #pragma unroll
+            for (int k = 0; k < V; ++k) part[q][k] = fmaf(v[j], x[j][q].v[k], part[q][k]);
+        if constexpr (F64) {
+    #pragma unroll
+          for (int q = 0; q < CPL; ++q)
+    #pragma unroll
+            for (int k = 0; k < V; ++k) {
+              acc[q][k] += (double)part[q][k];
+              part[q][k] = 0.f;
+            }
+        } else if constexpr (TWO) {
+          constexpr int WS = 32 / E;            // steps per 32-entry window
+          if (s % WS == WS - 1) {
+    #pragma unroll
+            for (int q = 0; q < CPL; ++q)
+    #pragma unroll
+              for (int k = 0; k < V; ++k) {
+                acc2[q][k] += part[q][k];
+                part[q][k] = 0.f;
+              }
+          }
+        }
+      }
+      __syncwarp(gmask);
+      issue(w + 2);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   }
   if constexpr (TWO) {
 #pragma unroll
@@ -344,11 +435,11 @@ int bucket_of(int32_t len) {
 }
 
 template <int G, int CPL, bool F64, int V, int MB = Tune<CPL, V>::MINB,
-          int EE = Tune<CPL, V>::E, bool TWO = false>
+          int EE = Tune<CPL, V>::E, bool TWO = false, bool STG = false>
 void launch_spmm(const SpmmArgs& a, int nslabs, cudaStream_t s) {
   const int64_t threads = a.n_items * G;
   const unsigned gx = (unsigned)((threads + 255) / 256);
-  spmm_kernel<G, CPL, F64, V, MB, EE, TWO><<<dim3(gx, nslabs), 256, 0, s>>>(a);
+  spmm_kernel<G, CPL, F64, V, MB, EE, TWO, STG><<<dim3(gx, nslabs), 256, 0, s>>>(a);
 }
 
 using LaunchFn = void (*)(const SpmmArgs&, int, cudaStream_t);
@@ -392,6 +483,17 @@ LaunchFn pick_exp(int G, int MB, int E, bool two) {
                : &launch_spmm<g, 1, true, 8, m, e, false>;
   DG_CASE(8, 3, 2) DG_CASE(8, 4, 2) DG_CASE(16, 3, 2) DG_CASE(16, 4, 2)
   DG_CASE(8, 3, 4) DG_CASE(8, 4, 4) DG_CASE(16, 3, 4) DG_CASE(16, 4, 4)
+#undef DG_CASE
+  return nullptr;
+}
+
+LaunchFn pick_stg(int G, int MB, int E, bool two) {
+#define DG_CASE(g, m, e)                                                 \
+  if (G == g && MB == m && E == e)                                       \
+    return two ? &launch_spmm<g, 1, false, 8, m, e, true, true>          \
+               : &launch_spmm<g, 1, true, 8, m, e, false, true>;
+  DG_CASE(8, 3, 4) DG_CASE(8, 4, 4) DG_CASE(16, 3, 4) DG_CASE(16, 4, 4)
+  DG_CASE(8, 3, 2) DG_CASE(8, 4, 2) DG_CASE(16, 3, 2) DG_CASE(16, 4, 2)
 #undef DG_CASE
   return nullptr;
 }
@@ -746,6 +848,9 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   static const int env_two = env_int("DG_SPMM_TWO", 0);
   if (v8 && acc && CPL == 1 && (env_e || env_two))
     fn = pick_exp(G, minb ? minb : 3, env_e ? env_e : 4, env_two != 0);
+  static const int env_stg = env_int("DG_SPMM_STG", 0);
+  if (v8 && acc && CPL == 1 && env_stg)
+    fn = pick_stg(G, minb ? minb : 3, env_e ? env_e : 4, env_two != 0);
   if (!fn) return set_err(DG_ERR_ARG, "dg_spmm_run: no kernel for config");
   fn(a, ns, S(stream));
   DG_LAUNCHED();
