@@ -487,6 +487,21 @@ LaunchFn pick_exp(int G, int MB, int E, bool two) {
   return nullptr;
 }
 
+// acc == 2 (the default): one 256-bit chunk per lane, entries staged in
+// shared memory, two-level fp32 sums, 4 CTAs/SM at 2 entries per step
+// (64 registers, no spill).  Sweep (profiles/r01/spmm_sweep_stg.txt): f=602
+// 19.8 -> 18.2 ms, f=41 1.95 -> 1.77 ms, products f=100 6.4 -> 6.1 ms.
+LaunchFn pick_two(int G) {
+  switch (G) {
+    case 2: return &launch_spmm<2, 1, false, 8, 4, 2, true, true>;
+    case 4: return &launch_spmm<4, 1, false, 8, 4, 2, true, true>;
+    case 8: return &launch_spmm<8, 1, false, 8, 4, 2, true, true>;
+    case 16: return &launch_spmm<16, 1, false, 8, 4, 2, true, true>;
+    case 32: return &launch_spmm<32, 1, false, 8, 4, 2, true, true>;
+    default: return nullptr;
+  }
+}
+
 LaunchFn pick_stg(int G, int MB, int E, bool two) {
 #define DG_CASE(g, m, e)                                                 \
   if (G == g && MB == m && E == e)                                       \
@@ -774,8 +789,8 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
                 float* const* z, int32_t f, int64_t ld_h, int64_t ld_z, int32_t acc,
                 int32_t slab_floats, int32_t beta, void* stream) {
   if (!p) return set_err(DG_ERR_ARG, "dg_spmm_run: null plan");
-  if (f < 1 || ld_h % 4 || ld_z % 4 || f > ld_h || f > ld_z)
-    return set_err(DG_ERR_ARG, "dg_spmm_run: need 1 <= f <= ld, ld % 4 == 0");
+  if (f < 1 || ld_h % 4 || ld_z % 4 || f > ld_h || f > ld_z || acc < 0 || acc > 2)
+    return set_err(DG_ERR_ARG, "dg_spmm_run: need 1 <= f <= ld, ld % 4 == 0, acc in 0..2");
   // 256-bit lane chunks when rows are >= 32 floats and 32-B aligned
   bool v8 = f > 16 && ld_h % 8 == 0 && ld_z % 8 == 0;
   for (int r = 0; r < p->n_ranks && v8; ++r) {
@@ -826,6 +841,17 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   static const int force_g = env_int("DG_SPMM_FORCE_G", 0);
   static const int force_c = env_int("DG_SPMM_FORCE_CPL", 0);
   static const int minb = env_int("DG_SPMM_MINB", 0);
+  const bool two = acc == 2 && v8;
+  if (two) {
+    // one chunk per lane (the two-level kernel's shape): the narrowest
+    // power-of-two group covering a slab, same number of slabs
+    int g = 2;
+    while (g < (chunks + ns - 1) / ns && g < 32) g <<= 1;
+    if (g * ns >= chunks) {
+      G = g;
+      CPL = 1;
+    }
+  }
   if (force_g > 0 && force_c > 0) {
     G = force_g;
     CPL = force_c;
@@ -843,6 +869,7 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   if (p->n_items == 0) return DG_OK;
   LaunchFn fn = v8 ? (acc ? pick_launch<true, 8>(G, CPL) : pick_launch<false, 8>(G, CPL))
                    : (acc ? pick_launch<true, 4>(G, CPL) : pick_launch<false, 4>(G, CPL));
+  if (two && CPL == 1) fn = pick_two(G);
   if (v8 && acc && CPL == 1 && minb >= 3) fn = pick_minb(G, minb);
   static const int env_e = env_int("DG_SPMM_E", 0);
   static const int env_two = env_int("DG_SPMM_TWO", 0);

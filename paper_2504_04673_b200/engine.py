@@ -30,9 +30,10 @@ import torch
 from . import _lib as L
 
 __all__ = ["DevicePlan", "single_spmm", "device_gemm", "reduce_members", "pad4", "to_device",
-           "ACC_FP64"]
+           "ACC_FP64", "ACC_TWO_LEVEL"]
 
-ACC_FP64 = 1          # accumulate SpMM in fp64 (fp32 inputs / outputs)
+ACC_FP64 = 1          # fp32 4-entry windows folded into fp64 accumulators
+ACC_TWO_LEVEL = 2     # two-level fp32 (<= 64 ulp of sum|terms| per item; rows >= 32 floats)
 MAX_CHUNK = 1024      # nonzeros per work item before a row is split
 
 
@@ -170,8 +171,8 @@ class DevicePlan:
     exchange + device barrier run on a side stream, and a halo (boundary)
     pass that accumulates into Z once the barrier has passed."""
 
-    def __init__(self, vplan, local_ranks=None, acc=ACC_FP64, max_chunk=MAX_CHUNK, max_ld=None,
-                 standalone=False, parities=2):
+    def __init__(self, vplan, local_ranks=None, acc=ACC_TWO_LEVEL, max_chunk=MAX_CHUNK,
+                 max_ld=None, standalone=False, parities=2):
         from .dist import world
         lib = L.lib()
         self.vplan = vplan
