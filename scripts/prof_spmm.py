@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--workload", default="reddit")
     ap.add_argument("--f", type=int, nargs="+", default=[602])
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--acc", type=int, nargs="+", default=[1])
+    ap.add_argument("--acc", type=int, nargs="+", default=[2])
     ap.add_argument("--slab", type=int, nargs="+", default=[0])
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--ld-align", type=int, default=0)
