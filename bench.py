@@ -338,9 +338,15 @@ def run_papers(args, wl):
     l0 = _lib.launch_count()
     clk = ClockSampler(torch.cuda.current_device())
     holder = {}
+    gr.timer = PhaseTimer()                 # per-epoch device times inside the timed region
     ms_epoch = _timed(lambda: holder.__setitem__("run", gr.run(args.steps)), 1, w) / args.steps
     clocks = clk.stop()
     launches = _lib.launch_count() - l0
+    torch.cuda.synchronize()
+    ev = [e for name, e in gr.timer.events if name == "epoch_start"]
+    end = gr.timer.events[-1][1]
+    each = [a.elapsed_time(b) for a, b in zip(ev, ev[1:] + [end])]
+    gr.timer = None
     res = gr.result(holder["run"], args.steps)
     peak_mem = max(w.all_gather_object(torch.cuda.max_memory_allocated()))
     gr.timer = PhaseTimer()
@@ -420,6 +426,7 @@ def run_papers(args, wl):
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
         "epoch_breakdown_ms": breakdown,
+        "epoch_ms_each_rank0": [round(x, 2) for x in each],
         "peak_mem_gib": round(peak_mem / 2**30, 1),
         "setup_s": round(t_setup, 1),
         "clocks": clocks,
