@@ -346,6 +346,13 @@ def run_papers(args, wl):
     ev = [e for name, e in gr.timer.events if name == "epoch_start"]
     end = gr.timer.events[-1][1]
     each = [a.elapsed_time(b) for a, b in zip(ev, ev[1:] + [end])]
+    slow = {}                               # phases of the slowest timed epoch
+    k = int(np.argmax(each))
+    marks = gr.timer.events
+    starts = [i for i, (nm, _) in enumerate(marks) if nm == "epoch_start"] + [len(marks)]
+    seg = marks[starts[k]:starts[k + 1]]
+    for (_, e0), (nm, e1) in zip(seg[:-1], seg[1:]):
+        slow[nm] = round(slow.get(nm, 0.0) + e0.elapsed_time(e1), 2)
     gr.timer = None
     res = gr.result(holder["run"], args.steps)
     peak_mem = max(w.all_gather_object(torch.cuda.max_memory_allocated()))
@@ -427,6 +434,8 @@ def run_papers(args, wl):
         "gpu_launches": int(launches),
         "epoch_breakdown_ms": breakdown,
         "epoch_ms_each_rank0": [round(x, 2) for x in each],
+        "epoch_ms_median_rank0": round(float(np.median(each)), 2),
+        "slowest_epoch_breakdown_ms": slow,
         "peak_mem_gib": round(peak_mem / 2**30, 1),
         "setup_s": round(t_setup, 1),
         "clocks": clocks,

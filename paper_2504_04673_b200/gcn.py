@@ -221,6 +221,30 @@ def _check_train_inputs(features, labels, train_mask):
     return labels, mask
 
 
+class _Arena:
+    """Per-rank activation buffers reused across epochs (one flat buffer per
+    slot, grown only when a larger view is requested).  At papers scale the
+    epoch's four ~20 GB activations would otherwise be fresh caching-allocator
+    requests every epoch -- occasionally several seconds of allocator
+    recovery.  Slot lifetimes (gcn.py:270-285): "t" the forward SpMM output
+    (consumed by that layer's transform), "l" the logits (until the loss),
+    then the backward SpMM outputs (the logits are dead by then), "g" the
+    loss gradient."""
+
+    def __init__(self, device):
+        self.device = device
+        self.bufs = {}
+
+    def get(self, slot, rows, ld):
+        need = rows * ld
+        buf = self.bufs.get(slot)
+        if buf is None or buf.numel() < need:
+            self.bufs[slot] = buf = None
+            buf = self.bufs[slot] = torch.empty(max(need, 4), dtype=torch.float32,
+                                                device=self.device)
+        return buf[:need].view(rows, ld)
+
+
 class _Dense:
     """The GCN step's dense transforms on the library's kernels
     (dg_dense_rows / dg_dense_tn); cuBLAS (torch.mm, TF32 off) only for
@@ -234,13 +258,15 @@ class _Dense:
     def _rows_ok(K, N):
         return N <= 64 and K * 16 * ((N + 15) // 16) <= 16384
 
-    def fwd(self, t, w, f_in, f_out, relu):
-        """z = t @ w (padded), h = relu(z) if requested (gcn.py:274-276)."""
+    def fwd(self, t, w, f_in, f_out, relu, z=None):
+        """z = t @ w (padded), h = relu(z) if requested (gcn.py:274-276);
+        `z` optionally preallocated (n x ld_out)."""
         n, ldo = t.shape[0], w.shape[1]
         if not self._rows_ok(f_in, f_out):
-            z = torch.mm(t, w)
+            z = torch.mm(t, w) if z is None else torch.mm(t, w, out=z)
             return z, (torch.clamp_min(z, 0.0) if relu else None)
-        z = torch.empty((n, ldo), dtype=torch.float32, device=self.device)
+        if z is None:
+            z = torch.empty((n, ldo), dtype=torch.float32, device=self.device)
         h = torch.empty_like(z) if relu else None
         L.check(L.lib().dg_dense_rows(t.data_ptr(), t.stride(0), n, f_in, w.data_ptr(),
                                       w.stride(0), f_out, 0, z.data_ptr(), ldo,
@@ -371,6 +397,10 @@ class GcnRun:
         ws = [w.clone() for w in self.w0] if weights_out is None else weights_out
         xent = self.xent.setdefault(comm.rank, _Xent(r1 - r0, self.device))
         dense = self.dense.setdefault(comm.rank, _Dense(self.device))
+        if not hasattr(self, "arena"):
+            self.arena = {}
+        arena = self.arena.setdefault(comm.rank, _Arena(self.device))
+        n_i = r1 - r0
         exchange_index_lists(comm, dm.fwd, cfg.variant)
         if dm.bwd is not dm.fwd:
             exchange_index_lists(comm, dm.bwd, cfg.variant)
@@ -409,20 +439,23 @@ class GcnRun:
                             L.check(lib.dg_relu(z.data_ptr(), h.data_ptr(), z.shape[0],
                                                 dims[l + 1], lds[l + 1], st))
                     else:
-                        t = spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant)
+                        t = spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant,
+                                       out=arena.get("t", n_i, lds[l]))
                         mark(f"fwd_spmm_f{dims[l]}")
-                        z, h = dense.fwd(t, w, dims[l], dims[l + 1], l < last)
+                        z, h = dense.fwd(t, w, dims[l], dims[l + 1], l < last,
+                                         z=arena.get("l", n_i, lds[l + 1]) if l == last else None)
                     zs.append(z)
                     hs.append(h if l < last else z)
                     mark(f"fwd_dense_{l}")
                 logits = hs[-1]
                 t = u = parts = z = h = None      # only hs / zs stay alive (HBM at scale)
-                g = torch.empty_like(logits)
+                g = arena.get("g", logits.shape[0], logits.shape[1])
                 xent(logits, dims[-1], yb, mb, self.denom, g, stats[epoch])
                 mark("xent")
                 hs[-1] = zs[-1] = logits = None       # not needed by the backward pass
                 for l in range(last, -1, -1):
-                    m = spmm_phase(comm, dm.bwd, g, dims[l + 1], cfg.variant)
+                    m = spmm_phase(comm, dm.bwd, g, dims[l + 1], cfg.variant,
+                                   out=arena.get("l", n_i, lds[l + 1]))   # logits are dead
                     mark(f"bwd_spmm_f{dims[l + 1]}")
                     y = comm.all_reduce_sum(dense.wgrad(hs[l], m, dims[l], dims[l + 1], lds[l],
                                                         lds[l + 1]),
