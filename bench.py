@@ -412,7 +412,7 @@ def run_papers(args, wl):
         "metric": "gcn_epoch_ms", "value": round(ms_epoch, 3), "unit": "ms",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_epoch, 3), "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32 (SpMM accumulates f64)", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": wl["desc"], "variant": args.variant, "p": p, "c": 1,
                    "partition": "block (partition.py:154-161)",
                    "l2": "inputs larger than L2 (H0 = %d MB per GPU)"
@@ -623,7 +623,7 @@ def run_ours(args, wl):
         "metric": "gcn_epoch_ms", "value": round(ms_epoch, 3), "unit": "ms",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_epoch, 3), "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f32 (SpMM accumulates f64)", "data": "synthetic",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": wl["desc"], "variant": args.variant, "p": p, "c": c,
                    "reduce_after_transform": bool(args.reduce_after_transform),
                    "partition": part_name,

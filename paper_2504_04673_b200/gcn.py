@@ -10,7 +10,8 @@ the column group, `G = (M W^T) * 1[Z > 0]` with W before its update, and
 SGD.  Every rank's data stays on the GPU for the whole run; loss and
 accuracy are accumulated on the device and read back once at the end.
 
-Numerics: fp32 storage, SpMM accumulated in fp64, GEMMs on cuBLAS fp32
+Numerics: fp32 storage; SpMM sums in fp32 windows folded into a second fp32
+(rows >= 32 floats) or fp64 (narrower rows) accumulator; GEMMs fp32
 with TF32 off.  Widths are padded to multiples of 4 (zero padding, also in
 the weights) so every activation is a 16-byte-aligned row-major tensor.
 """
