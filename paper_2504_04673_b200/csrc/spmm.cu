@@ -792,7 +792,8 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   if (f < 1 || ld_h % 4 || ld_z % 4 || f > ld_h || f > ld_z || acc < 0 || acc > 2)
     return set_err(DG_ERR_ARG, "dg_spmm_run: need 1 <= f <= ld, ld % 4 == 0, acc in 0..2");
   // 256-bit lane chunks when rows are >= 32 floats and 32-B aligned
-  bool v8 = f > 16 && ld_h % 8 == 0 && ld_z % 8 == 0;
+  static const int v8_16 = env_int("DG_SPMM_V8_16", 0);   // sweep: 256-bit lanes at f <= 16
+  bool v8 = (f > 16 || (v8_16 && f > 8)) && ld_h % 8 == 0 && ld_z % 8 == 0;
   for (int r = 0; r < p->n_ranks && v8; ++r) {
     const uintptr_t al = (uintptr_t)h_local[r] | (uintptr_t)z[r] |
                          (uintptr_t)(h_halo ? h_halo[r] : nullptr);
