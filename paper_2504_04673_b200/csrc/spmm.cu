@@ -407,165 +407,6 @@ __global__ void __launch_bounds__(256, MB)
   }
 }
 
-// GATH (acc == 2, 256-bit lanes, one chunk per lane): the gathered H-row
-// chunks land in shared memory by cp.async -- each lane copies its own
-// 32 B of every entry's row and later reads back only those bytes, so no
-// cross-lane synchronisation is needed -- with D steps in flight.  The
-// in-flight rows no longer occupy registers: MLP is bounded by shared
-// memory (D x 2 entries x 32 B per thread) instead of the register file.
-// Entries are staged as in the STG form; numerics are the two-level fp32
-// sums (32-entry windows).
-constexpr int GATH_D = 4;                   // steps in flight per lane
-
-template <int G, int D>
-__global__ void __launch_bounds__(256, 3) spmm_gather_kernel(const __grid_constant__ SpmmArgs a) {
-  constexpr int E = 2, WIN = 2 * G, S = WIN / E;
-  static_assert(S >= 2 * D - 1, "an entry window must outlast the gather pipeline");
-  __shared__ __align__(16) int2 stg[256 / G][2][WIN];
-  extern __shared__ __align__(16) float4 ring[];   // [D][E][2][256]
-  const int tid = threadIdx.x;
-  const int lig = tid & (G - 1);
-  const int grp = tid / G;
-  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + tid) / G;
-  if (gid >= a.n_items) return;             // whole group leaves together
-  const Item it = a.items[gid];
-  const RankArgs& R = a.r[it.rank];
-  const int chk = blockIdx.y * a.slab + lig;
-  const bool on = chk < a.chunks && lig < a.slab;
-  const int64_t ld = a.ld_h;
-  const float* __restrict__ hl = R.hl;
-  const float* __restrict__ hh = R.hh;
-  const int64_t nl = R.n_local;
-  const unsigned gmask = G == 32 ? 0xffffffffu
-                                 : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
-  const int2* __restrict__ src = reinterpret_cast<const int2*>(R.ent) + it.lo;
-  const int len = it.len;
-  const int steps = (len + E - 1) / E;
-  const int nwin = (len + WIN - 1) / WIN;
-  const int len2 = (len + 1) & ~1;
-  auto issue_win = [&](int w) {
-    const int e0 = w * WIN + 2 * lig;
-    int2* dst = &stg[grp][w & 1][2 * lig];
-    if (w < nwin && e0 < len2) {
-      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(src + e0)
-                   : "memory");
-    } else {
-      *reinterpret_cast<int4*>(dst) = make_int4(0, 0, 0, 0);
-    }
-  };
-  auto slot = [&](int stage, int j, int h) -> float4* {
-    return ring + ((stage * E + j) * 2 + h) * 256 + tid;
-  };
-  float part[8], acc2[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) part[k] = acc2[k] = 0.f;
-  float vals[D][E];
-  issue_win(0);
-  issue_win(1);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncwarp(gmask);
-  const int total = steps + D - 1;
-  for (int s0 = 0; s0 < total; s0 += D) {
-#pragma unroll
-    for (int u = 0; u < D; ++u) {
-      const int s = s0 + u;                 // issue step s into stage u (= s % D)
-      if (s < steps) {
-        const int2* win = stg[grp][(s / S) & 1];
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-          const int e = s * E + j;
-          const int2 en = win[e % WIN];
-          vals[u][j] = e < len ? __int_as_float(en.y) : 0.f;
-          if (e < len && on) {
-            const int c = en.x;
-            const float* hp = (c < nl ? hl + (int64_t)c * ld : hh + (int64_t)(c - nl) * ld) +
-                              (int64_t)chk * 8;
-            const unsigned s0a = (unsigned)__cvta_generic_to_shared(slot(u, j, 0));
-            const unsigned s1a = (unsigned)__cvta_generic_to_shared(slot(u, j, 1));
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s0a), "l"(hp)
-                         : "memory");
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s1a), "l"(hp + 4)
-                         : "memory");
-          }
-        }
-        // the lagging consumer has left window w-1 by step w*S + D - 1:
-        // refill that buffer with window w+1
-        if (s % S == D - 1 && s >= S) {
-          __syncwarp(gmask);
-          issue_win(s / S + 1);
-        }
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-      const int c = s - (D - 1);            // consume step c from stage (u + 1) % D
-      if (c >= 0 && c < steps) {
-        asm volatile("cp.async.wait_group %0;" ::"n"(D - 1) : "memory");
-        __syncwarp(gmask);                  // entry windows written by other lanes
-        const int cu = (u + 1) % D;         // static after unrolling
-        if (on) {
-#pragma unroll
-          for (int j = 0; j < E; ++j) {
-            if (c * E + j < len) {
-              const float4 a0 = *slot(cu, j, 0);
-              const float4 a1 = *slot(cu, j, 1);
-              const float v = vals[cu][j];
-              part[0] = fmaf(v, a0.x, part[0]);
-              part[1] = fmaf(v, a0.y, part[1]);
-              part[2] = fmaf(v, a0.z, part[2]);
-              part[3] = fmaf(v, a0.w, part[3]);
-              part[4] = fmaf(v, a1.x, part[4]);
-              part[5] = fmaf(v, a1.y, part[5]);
-              part[6] = fmaf(v, a1.z, part[6]);
-              part[7] = fmaf(v, a1.w, part[7]);
-            }
-          }
-        }
-        if (c % 16 == 15) {                 // 32-entry window
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            acc2[k] += part[k];
-            part[k] = 0.f;
-          }
-        }
-      }
-    }
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  if (!on) return;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) part[k] += acc2[k];
-  if (it.slot < 0) {
-    float4* zq = reinterpret_cast<float4*>(R.z + (int64_t)it.row * a.ld_z + (int64_t)chk * 8);
-    if (a.beta) {
-      const float4 z0 = zq[0], z1 = zq[1];
-      part[0] += z0.x; part[1] += z0.y; part[2] += z0.z; part[3] += z0.w;
-      part[4] += z1.x; part[5] += z1.y; part[6] += z1.z; part[7] += z1.w;
-    }
-    zq[0] = make_float4(part[0], part[1], part[2], part[3]);
-    zq[1] = make_float4(part[4], part[5], part[6], part[7]);
-  } else {
-    double4* dq = reinterpret_cast<double4*>(a.part + (int64_t)it.slot * a.ld_part +
-                                             (int64_t)chk * 8);
-    dq[0] = make_double4(part[0], part[1], part[2], part[3]);
-    dq[1] = make_double4(part[4], part[5], part[6], part[7]);
-  }
-}
-
-template <int G>
-void launch_gather(const SpmmArgs& a, int nslabs, cudaStream_t s) {
-  const int64_t threads = a.n_items * G;
-  const unsigned gx = (unsigned)((threads + 255) / 256);
-  const size_t smem = (size_t)GATH_D * 2 * 2 * 256 * sizeof(float4);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(spmm_gather_kernel<G, GATH_D>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  spmm_gather_kernel<G, GATH_D><<<dim3(gx, nslabs), 256, smem, s>>>(a);
-}
-
 struct FixArgs {
   float* z[DG_MAX_LOCAL];
   const Fixup* fix;
@@ -670,15 +511,6 @@ LaunchFn pick_stg(int G, int MB, int E, bool two) {
   DG_CASE(8, 3, 2) DG_CASE(8, 4, 2) DG_CASE(16, 3, 2) DG_CASE(16, 4, 2)
 #undef DG_CASE
   return nullptr;
-}
-
-LaunchFn pick_gather(int G) {
-  switch (G) {
-    case 8: return &launch_gather<8>;
-    case 16: return &launch_gather<16>;
-    case 32: return &launch_gather<32>;
-    default: return nullptr;                // S = G steps per window must be >= 2D - 1
-  }
 }
 
 // Lane-group size G and chunks-per-lane CPL for `chunks` float4 chunks when
@@ -1045,8 +877,6 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   LaunchFn fn = v8 ? (acc ? pick_launch<true, 8>(G, CPL) : pick_launch<false, 8>(G, CPL))
                    : (acc ? pick_launch<true, 4>(G, CPL) : pick_launch<false, 4>(G, CPL));
   if (two && CPL == 1) fn = pick_two(G);
-  static const int env_gath = env_int("DG_SPMM_GATH", 0);
-  if (two && CPL == 1 && env_gath && pick_gather(G)) fn = pick_gather(G);
   if (v8 && acc && CPL == 1 && minb >= 3) fn = pick_minb(G, minb);
   static const int env_e = env_int("DG_SPMM_E", 0);
   static const int env_two = env_int("DG_SPMM_TWO", 0);
