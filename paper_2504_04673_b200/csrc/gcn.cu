@@ -130,7 +130,8 @@ __device__ __forceinline__ int grp_min(int v) {
 // xent_kernel (rows in order per group, groups in order per CTA, CTAs in
 // order in the last CTA).
 template <int G, int K>
-__global__ void __launch_bounds__(256) xent_vec_kernel(
+// 3 CTAs/SM for rows <= 256 classes (C=172: 20.9 -> 17.5 ms at 27.8M rows)
+__global__ void __launch_bounds__(256, (K <= 2 ? 3 : 1)) xent_vec_kernel(
     const float* __restrict__ x, int64_t n, int C, int64_t ld, const int64_t* __restrict__ labels,
     const uint8_t* __restrict__ mask, double denom, float* __restrict__ grad, int64_t ldg,
     double* scratch, unsigned* counter, double* out) {
@@ -182,7 +183,10 @@ __global__ void __launch_bounds__(256) xent_vec_kernel(
         for (int e = 0; e < 4; ++e) m = fmaxf(m, v[u][k][e]);
       m = grp_max<G>(m);
       const int64_t lbl = labels[row];
-      double s = 0.0, xl = 0.0;
+      // per lane: an fp32 partial of its <= 4K exponentials (each in (0, 1]),
+      // then the lanes' partials summed in fp64
+      float sl = 0.f;
+      double xl = 0.0;
       int am = C;
 #pragma unroll
       for (int k = 0; k < K; ++k)
@@ -193,18 +197,19 @@ __global__ void __launch_bounds__(256) xent_vec_kernel(
             if (v[u][k][e] == m && j < am) am = j;
             if (j == lbl) xl = (double)v[u][k][e] - (double)m;
             v[u][k][e] = expf(v[u][k][e] - m);
-            s += (double)v[u][k][e];
+            sl += v[u][k][e];
           } else {
             v[u][k][e] = 0.f;
           }
         }
-      s = grp_sum<G>(s);
+      const double s = grp_sum<G>((double)sl);
       xl = grp_sum<G>(xl);
       am = grp_min<G>(am);
       const bool on = valid[u] && mask[row] != 0;
       // (softmax - onehot) / denom with one division per row: p_j/denom =
       // e_j * (1 / (s * denom)); the label term subtracts 1/denom
       const double scale = 1.0 / (s * denom);
+      const float scale_f = (float)scale;
       const double inv_d = 1.0 / denom;
       float4* gr = reinterpret_cast<float4*>(grad + row * ldg);
 #pragma unroll
@@ -215,9 +220,11 @@ __global__ void __launch_bounds__(256) xent_vec_kernel(
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int j = 4 * c + e;
-            double sm = (double)v[u][k][e] * scale;
-            if (j == lbl) sm -= inv_d;
-            o[e] = (on && j < C) ? (float)sm : 0.f;
+            // fp32 product (<= 1.5 ulp); the label entry, where p - 1 may
+            // cancel, in fp64
+            float sm = v[u][k][e] * scale_f;
+            if (j == lbl) sm = (float)((double)v[u][k][e] * scale - inv_d);
+            o[e] = (on && j < C) ? sm : 0.f;
           }
           gr[c] = make_float4(o[0], o[1], o[2], o[3]);
         }
@@ -310,7 +317,7 @@ int dg_xent(const float* logits, int64_t n, int32_t C, int64_t ld, const int64_t
   const int K = (nchunk + G - 1) / G;
   if (vec && K <= 4) {
     const int rpb = (256 / G) * 4;                   // rows per CTA step (RU = 4)
-    const unsigned blocks = (unsigned)std::min<int64_t>((n + rpb - 1) / rpb, 8 * 148);
+    const unsigned blocks = (unsigned)std::min<int64_t>((n + rpb - 1) / rpb, 12 * 148);
     cudaStream_t st = S(stream);
 #define DG_XV(g, k) xent_vec_kernel<g, k><<<blocks, 256, 0, st>>>(logits, n, C, ld, labels, mask, \
                                                                   denom, grad, ld_grad, scratch, \
