@@ -129,8 +129,8 @@ __device__ __forceinline__ int grp_min(int v) {
 // expf per element).  Same numerics and deterministic reduction order as
 // xent_kernel (rows in order per group, groups in order per CTA, CTAs in
 // order in the last CTA).
+// 3 CTAs/SM for rows <= 256 classes (C=172: 20.9 -> 17.5 ms at 27.8M rows).
 template <int G, int K>
-// 3 CTAs/SM for rows <= 256 classes (C=172: 20.9 -> 17.5 ms at 27.8M rows)
 __global__ void __launch_bounds__(256, (K <= 2 ? 3 : 1)) xent_vec_kernel(
     const float* __restrict__ x, int64_t n, int C, int64_t ld, const int64_t* __restrict__ labels,
     const uint8_t* __restrict__ mask, double denom, float* __restrict__ grad, int64_t ldg,
