@@ -792,13 +792,13 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   if (f < 1 || ld_h % 4 || ld_z % 4 || f > ld_h || f > ld_z || acc < 0 || acc > 2)
     return set_err(DG_ERR_ARG, "dg_spmm_run: need 1 <= f <= ld, ld % 4 == 0, acc in 0..2");
   // 256-bit lane chunks when rows are >= 32 floats and 32-B aligned
-  // 256-bit lanes for rows of >= 32 floats, and for 9..16-float rows when the
-  // gathered table does not fit the L2 budget (DRAM-resident gathers: products
-  // f=16 1.55 -> 1.27 ms; an L2-resident table keeps 128-bit lanes: Reddit f=16
-  // 0.71 vs 0.78 ms; profiles/r01/spmm_f16_lanes.txt)
+  // 256-bit lanes for rows of >= 32 floats, and for 9..16-float rows gathered
+  // from a table far larger than L2 (papers-shaped f=16: 55.7 -> 53.0 ms at
+  // N=4).  Tables near L2 size keep 128-bit lanes (Reddit f=16 0.71 vs 0.78 ms;
+  // products N=4 halo pass 0.62 vs 0.90 ms; profiles/r01/spmm_f16_lanes.txt)
   int64_t ext_rows_all = 0;
   for (int r = 0; r < p->n_ranks; ++r) ext_rows_all += p->ext_rows[r];
-  const bool dram_table = (double)ext_rows_all * (double)ld_h * 4.0 > 64.0 * 1024 * 1024;
+  const bool dram_table = (double)ext_rows_all * (double)ld_h * 4.0 > 1024.0 * 1024 * 1024;
   bool v8 = (f > 16 || (f > 8 && acc == 2 && dram_table)) && ld_h % 8 == 0 && ld_z % 8 == 0;
   for (int r = 0; r < p->n_ranks && v8; ++r) {
     const uintptr_t al = (uintptr_t)h_local[r] | (uintptr_t)z[r] |
