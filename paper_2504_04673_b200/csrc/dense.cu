@@ -230,13 +230,21 @@ __global__ void __launch_bounds__(256) dense_tn_kernel(
   }
 }
 
+// One warp per output element: lane l sums slices l, l+32, ... in order,
+// then a fixed xor tree -- deterministic, and the slices' partials are read
+// 32 at a time instead of one dependent load per slice.
 __global__ void dense_tn_reduce_kernel(const double* __restrict__ work, int slices, int K, int NP,
                                        int N, float* __restrict__ Y, int64_t ldy) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < K * NP; i += gridDim.x * blockDim.x) {
-    const int k = i / NP, j = i % NP;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < (int64_t)K * NP;
+       i += nw) {
     double s = 0.0;
-    for (int p = 0; p < slices; ++p) s += work[(int64_t)p * K * NP + i];
-    if (j < ldy) Y[(int64_t)k * ldy + j] = (j < N) ? (float)s : 0.f;
+    for (int p = lane; p < slices; p += 32) s += work[(int64_t)p * K * NP + i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const int k = (int)(i / NP), j = (int)(i % NP);
+    if (lane == 0 && j < ldy) Y[(int64_t)k * ldy + j] = (j < N) ? (float)s : 0.f;
   }
 }
 
@@ -311,8 +319,8 @@ int dg_dense_tn(const float* H, int64_t ldh, int64_t n, int32_t K, const float* 
     default: dense_tn_kernel<4><<<grid, 256, 0, st>>>(H, ldh, n, K, M, ldm, N, rows_per, work); break;
   }
   DG_LAUNCHED();
-  const int total = K * NPT;
-  dense_tn_reduce_kernel<<<(unsigned)std::min(1024, (total + 255) / 256), 256, 0, st>>>(
+  const int total = K * NPT;                        // one warp per output element
+  dense_tn_reduce_kernel<<<(unsigned)std::min(4096, (total + 7) / 8), 256, 0, st>>>(
       work, (int)slices, K, NPT, N, Y, ldy);
   DG_LAUNCHED();
   return DG_OK;
