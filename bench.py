@@ -227,7 +227,8 @@ def run_reference(args, wl):
     ms = statistics.median(vals[args.warmup:])
     line = {
         "metric": "gcn_epoch_ms", "value": round(ms, 3), "unit": "ms", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": wl["desc"], "variant": args.variant,

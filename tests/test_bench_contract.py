@@ -1,0 +1,35 @@
+"""bench.py's reference arm on CPU (no GPU needed): the contract's JSON
+line with impl=reference, the workload's metric/unit, a cpu_baseline that
+describes the run, and an e2e object carrying the same value."""
+
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_reference_arm_line_rmat14():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--workload", "rmat14", "--steps", "1", "--warmup", "1",
+                        "--ref-budget", "0.5"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    assert line["metric"] == "gcn_epoch_ms" and line["unit"] == "ms"
+    assert line["higher_is_better"] is False
+    assert line["value"] > 0 and line["ms_per_step"] == line["value"]
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] == 1 and cb["value"] == line["value"]
+    assert line["e2e"] == {"value": line["value"], "unit": "ms", "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+    assert "R-MAT" in line["config"]["workload"]
+
+
+def test_reference_arm_nonzero_rank_is_silent():
+    env = dict(os.environ, RANK="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--workload", "rmat14", "--gpus", "2"], capture_output=True, text=True,
+                       timeout=300, env=env)
+    assert r.returncode == 0 and r.stdout.strip() == ""
