@@ -7,23 +7,26 @@
 // Why this shape (DESIGN.md has the measurements):
 //  * SpMM is gather-bound (<= f/4 flop per byte), not tensor-core work.
 //    The limiter on B200 is memory-level parallelism: every nonzero needs
-//    its (col, val) from the CSR stream before the H row can be gathered.
+//    its (col, val) before its H row can be gathered, and the gathered rows
+//    wait in registers, so rows in flight per SM = warps x entries per step.
 //  * Entries are stored interleaved, 8 B per nonzero ({col, val}), each
-//    work item starting 16-B aligned, so a lane fetches two entries with
-//    one 16-B load.  All lanes of a group load the same entries (a uniform
-//    broadcast load, one L1 wavefront) -- no shuffles.  The next step's
-//    entries are prefetched while the current step's H rows are gathered
-//    (software pipelining hides the CSR stream latency).
-//  * A group of G lanes owns one item; lane l owns float4 chunks l, l+G, ...
-//    of the current feature slab, so one H-row gather is G x 16 B
-//    contiguous.  Wide layers are split into slabs (grid.y) sized so one
-//    slab of all gathered rows stays L2-resident; the CSR stream is loaded
-//    evict-first so it does not push H out of L2.
-//  * Numerics: each step's E products are summed in fp32 and folded into
-//    fp64 accumulators (error <= E * 2^-24 of the window's |terms|, E <= 8),
-//    in CSR storage order; long rows are split at fixed boundaries and the
-//    fp64 partials summed in chunk order.  Deterministic, and identical for
-//    every variant (aware == oblivious, 1.5D c=1 == 1D, bitwise).
+//    work item starting 16-B aligned.
+//  * A group of G lanes owns one item; lane l owns lane-chunks l, l+G, ...
+//    of the current feature slab, so one H-row gather is a G x 16 B (128-bit
+//    lanes) or G x 32 B (Blackwell 256-bit ld.global.nc.v8) contiguous
+//    request.  Wide layers are split into slabs (grid.y) sized so one slab of
+//    all gathered rows stays L2-resident; the CSR stream is evict-first.
+//  * Two forms.  acc = 1 (rows <= 16 floats): entries loaded with uniform
+//    16-B vector loads one step ahead, 4-entry fp32 windows folded into fp64
+//    accumulators.  acc = 2 (rows >= 32 floats, and 9..16-float rows of
+//    tables far larger than L2): one 256-bit chunk per lane, the item's
+//    entries staged in shared memory by cp.async one window ahead (no
+//    registers held by the prefetch), two-level fp32 sums (32-entry windows;
+//    <= 64 ulp of the row's sum of |terms| per 1024-entry item), 2 entries per
+//    step at 4 CTAs/SM with 64 registers.
+//  * Summation follows CSR storage order; long rows are split at fixed
+//    boundaries and the fp64 partials summed in chunk order.  Deterministic,
+//    and identical for every variant (aware == oblivious, 1.5D c=1 == 1D).
 
 #include "common.cuh"
 
