@@ -482,6 +482,60 @@ class GcnRun:
                            lambda comm: self.program(comm, epochs, stats[comm.rank]),
                            ctx=self.ctx)
 
+    def run_graph(self, epochs=None):
+        """`run` with the epoch captured once in a CUDA graph and replayed
+        (launch-bound small graphs, e.g. config 1).  Single
+        process, one rank, aggregate-first order.  The replayed epochs run
+        exactly the captured kernels on fixed buffers (inputs, activation
+        arena, weights updated in place); the ledger -- host bookkeeping --
+        is extended by the captured epoch's charges once per replay, so the
+        result equals `run` bit for bit (tests/test_gpu_api.py)."""
+        import copy
+        from .dist import world
+        epochs = self.cfg.epochs if epochs is None else epochs
+        if world().multi or self.grid.p != 1 or self.cfg.order != "aggregate-first":
+            raise ValueError("run_graph: single-process, single-rank, aggregate-first runs only")
+        dev = self.device
+        if getattr(self, "_graph", None) is None:
+            self._gw = [w.clone() for w in self.w0]
+            self._gstats = torch.zeros((1, 2), dtype=torch.float64, device=dev)
+            prog = lambda comm: self.program(comm, 1, self._gstats, weights_out=self._gw)  # noqa
+            run_program(1, 1, prog, ctx=self.ctx)          # warm-up: plans, arena, workspaces
+            torch.cuda.synchronize()
+            base = run_program(1, 1, lambda comm: self.program(comm, 0, self._gstats),
+                               ctx=self.ctx).ledger       # index setup only
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(torch.cuda.current_stream())
+            n0 = L.launch_count()
+            with torch.cuda.stream(side), torch.cuda.graph(g):
+                one = run_program(1, 1, prog, ctx=self.ctx).ledger
+            self._graph_launches = L.launch_count() - n0   # our kernels in one epoch
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            self._graph, self._gbase, self._gone = g, base, one
+        for w, w0 in zip(self._gw, self.w0):
+            w.copy_(w0)
+        stats = torch.zeros((max(epochs, 1), 2), dtype=torch.float64, device=dev)
+        for e in range(epochs):
+            self._gstats.zero_()                          # the loss kernel accumulates
+            self._graph.replay()
+            stats[e].copy_(self._gstats[0])
+        # ledger: index setup + epochs x the captured epoch's charges
+        led = copy.deepcopy(self._gbase)
+        base, one = self._gbase, self._gone
+        for e in range(epochs):
+            for prim, c in one.counters.items():
+                for k, arr in c.items():
+                    led.counters[prim][k] += arr - base.counters[prim][k]
+            led.wire_bytes_sent += one.wire_bytes_sent - base.wire_bytes_sent
+            led.marks[("epoch", e)] = led.snapshot()
+        led.pair_max_bytes = dict(one.pair_max_bytes)
+        led.pair_max_data_bytes = dict(one.pair_max_data_bytes)
+        from .runtime import RunResult
+        return RunResult([{"stats": stats, "weights": [w.clone() for w in self._gw]}], led,
+                         self.grid)
+
     def close(self):
         """Release the run's device state (collective under torchrun)."""
         for obj in self.ctx.values():
