@@ -410,194 +410,6 @@ __global__ void __launch_bounds__(256, MB)
   }
 }
 
-// TMA (experiment, DG_SPMM_TMA): each gathered row slab is fetched with ONE
-// bulk copy (cp.async.bulk, issued by the group's first lane) into a per-group
-// shared-memory ring of D steps, completion tracked by an mbarrier per stage;
-// lanes read their own 32 B back.  In-flight rows cost neither registers nor
-// per-lane load instructions.  Entries staged as in STG; two-level fp32 sums.
-constexpr int TMA_D = 4;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-
-template <int G, int D>
-__global__ void __launch_bounds__(256, 3) spmm_tma_kernel(const __grid_constant__ SpmmArgs a) {
-  constexpr int E = 2, WIN = 2 * G, S = WIN / E, GPB = 256 / G, SLAB = G * 32;
-  static_assert(S >= 2 * D - 1, "an entry window must outlast the pipeline");
-  __shared__ __align__(16) int2 stg[GPB][2][WIN];
-  __shared__ __align__(8) uint64_t bar[GPB][D];
-  extern __shared__ __align__(128) unsigned char ring[];   // [GPB][D][E][SLAB]
-  const int tid = threadIdx.x;
-  const int lig = tid & (G - 1);
-  const int grp = tid / G;
-  const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + tid) / G;
-  if (gid >= a.n_items) return;
-  const Item it = a.items[gid];
-  const RankArgs& R = a.r[it.rank];
-  const int slab0 = blockIdx.y * a.slab;
-  const int chk = slab0 + lig;
-  const bool on = chk < a.chunks && lig < a.slab;
-  const int act = min(a.slab, a.chunks - slab0);            // active chunks of this slab
-  const unsigned bytes = (unsigned)act * 32u;
-  const int64_t ld = a.ld_h;
-  const float* __restrict__ hl = R.hl;
-  const float* __restrict__ hh = R.hh;
-  const int64_t nl = R.n_local;
-  const unsigned gmask = G == 32 ? 0xffffffffu
-                                 : (((1u << G) - 1u) << ((tid & 31) & ~(G - 1)));
-  const int2* __restrict__ src = reinterpret_cast<const int2*>(R.ent) + it.lo;
-  const int len = it.len;
-  const int steps = (len + E - 1) / E;
-  const int nwin = (len + WIN - 1) / WIN;
-  const int len2 = (len + 1) & ~1;
-  unsigned char* myring = ring + (size_t)grp * D * E * SLAB;
-  auto issue_win = [&](int w) {
-    const int e0 = w * WIN + 2 * lig;
-    int2* dst = &stg[grp][w & 1][2 * lig];
-    if (w < nwin && e0 < len2) {
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)),
-                   "l"(src + e0) : "memory");
-    } else {
-      *reinterpret_cast<int4*>(dst) = make_int4(0, 0, 0, 0);
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  if (lig == 0) {
-#pragma unroll
-    for (int u = 0; u < D; ++u)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[grp][u])));
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  issue_win(0);
-  issue_win(1);
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncwarp(gmask);
-  float part[8], acc2[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) part[k] = acc2[k] = 0.f;
-  float vals[D][E];
-  const int total = steps + D - 1;
-  for (int s0 = 0; s0 < total; s0 += D) {
-#pragma unroll
-    for (int u = 0; u < D; ++u) {
-      const int s = s0 + u;
-      if (s < steps) {
-        if (s % S == 0 && s >= 2 * S) {     // entry window s / S (prefetched S - D + 1 steps ago)
-          asm volatile("cp.async.wait_group 0;" ::: "memory");
-          __syncwarp(gmask);
-        }
-        const int2* win = stg[grp][(s / S) & 1];
-        const float* rowp[E];
-        unsigned tx = 0;
-#pragma unroll
-        for (int j = 0; j < E; ++j) {
-          const int e = s * E + j;
-          const int2 en = win[e % WIN];
-          vals[u][j] = e < len ? __int_as_float(en.y) : 0.f;
-          rowp[j] = nullptr;
-          if (e < len) {
-            const int c = en.x;
-            rowp[j] = (c < nl ? hl + (int64_t)c * ld : hh + (int64_t)(c - nl) * ld) +
-                      (int64_t)slab0 * 8;
-            tx += bytes;
-          }
-        }
-        if (lig == 0) {
-          const unsigned b = smem_u32(&bar[grp][u]);
-          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
-                       "r"(tx) : "memory");
-#pragma unroll
-          for (int j = 0; j < E; ++j)
-            if (rowp[j])
-              asm volatile(
-                  "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes "
-                  "[%0], [%1], %2, [%3];" ::"r"(smem_u32(myring + (u * E + j) * SLAB)),
-                  "l"(rowp[j]), "r"(bytes), "r"(b)
-                  : "memory");
-        }
-        if (s % S == D - 1 && s >= S) {
-          __syncwarp(gmask);
-          issue_win(s / S + 1);
-        }
-      }
-      const int c = s - (D - 1);
-      if (c >= 0 && c < steps) {
-        const int cu = (u + 1) % D;
-        const unsigned b = smem_u32(&bar[grp][cu]);
-        const unsigned par = (unsigned)((c / D) & 1);
-        unsigned ok = 0;
-        while (!ok)
-          asm volatile(
-              "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
-              "selp.u32 %0, 1, 0, p; }"
-              : "=r"(ok)
-              : "r"(b), "r"(par)
-              : "memory");
-        if (on) {
-#pragma unroll
-          for (int j = 0; j < E; ++j) {
-            if (c * E + j < len) {
-              const float4* q =
-                  reinterpret_cast<const float4*>(myring + (cu * E + j) * SLAB + lig * 32);
-              const float4 a0 = q[0], a1 = q[1];
-              const float v = vals[cu][j];
-              part[0] = fmaf(v, a0.x, part[0]);
-              part[1] = fmaf(v, a0.y, part[1]);
-              part[2] = fmaf(v, a0.z, part[2]);
-              part[3] = fmaf(v, a0.w, part[3]);
-              part[4] = fmaf(v, a1.x, part[4]);
-              part[5] = fmaf(v, a1.y, part[5]);
-              part[6] = fmaf(v, a1.z, part[6]);
-              part[7] = fmaf(v, a1.w, part[7]);
-            }
-          }
-        }
-        __syncwarp(gmask);                  // stage cu may be refilled by the next issue
-        if (c % 16 == 15) {
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            acc2[k] += part[k];
-            part[k] = 0.f;
-          }
-        }
-      }
-    }
-  }
-  if (!on) return;
-#pragma unroll
-  for (int k = 0; k < 8; ++k) part[k] += acc2[k];
-  if (it.slot < 0) {
-    float4* zq = reinterpret_cast<float4*>(R.z + (int64_t)it.row * a.ld_z + (int64_t)chk * 8);
-    if (a.beta) {
-      const float4 z0 = zq[0], z1 = zq[1];
-      part[0] += z0.x; part[1] += z0.y; part[2] += z0.z; part[3] += z0.w;
-      part[4] += z1.x; part[5] += z1.y; part[6] += z1.z; part[7] += z1.w;
-    }
-    zq[0] = make_float4(part[0], part[1], part[2], part[3]);
-    zq[1] = make_float4(part[4], part[5], part[6], part[7]);
-  } else {
-    double4* dq = reinterpret_cast<double4*>(a.part + (int64_t)it.slot * a.ld_part +
-                                             (int64_t)chk * 8);
-    dq[0] = make_double4(part[0], part[1], part[2], part[3]);
-    dq[1] = make_double4(part[4], part[5], part[6], part[7]);
-  }
-}
-
-template <int G>
-void launch_tma(const SpmmArgs& a, int nslabs, cudaStream_t s) {
-  const int64_t threads = a.n_items * G;
-  const unsigned gx = (unsigned)((threads + 255) / 256);
-  const size_t smem = (size_t)(256 / G) * TMA_D * 2 * G * 32;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(spmm_tma_kernel<G, TMA_D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
-  spmm_tma_kernel<G, TMA_D><<<dim3(gx, nslabs), 256, smem, s>>>(a);
-}
-
 struct FixArgs {
   float* z[DG_MAX_LOCAL];
   const Fixup* fix;
@@ -702,15 +514,6 @@ LaunchFn pick_stg(int G, int MB, int E, bool two) {
   DG_CASE(8, 3, 2) DG_CASE(8, 4, 2) DG_CASE(16, 3, 2) DG_CASE(16, 4, 2)
 #undef DG_CASE
   return nullptr;
-}
-
-LaunchFn pick_tma(int G) {
-  switch (G) {
-    case 8: return &launch_tma<8>;
-    case 16: return &launch_tma<16>;
-    case 32: return &launch_tma<32>;
-    default: return nullptr;
-  }
 }
 
 // Lane-group size G and chunks-per-lane CPL for `chunks` float4 chunks when
@@ -1077,8 +880,6 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   LaunchFn fn = v8 ? (acc ? pick_launch<true, 8>(G, CPL) : pick_launch<false, 8>(G, CPL))
                    : (acc ? pick_launch<true, 4>(G, CPL) : pick_launch<false, 4>(G, CPL));
   if (two && CPL == 1) fn = pick_two(G);
-  static const int env_tma = env_int("DG_SPMM_TMA", 0);
-  if (two && CPL == 1 && env_tma && pick_tma(G)) fn = pick_tma(G);
   if (v8 && acc && CPL == 1 && minb >= 3) fn = pick_minb(G, minb);
   static const int env_e = env_int("DG_SPMM_E", 0);
   static const int env_two = env_int("DG_SPMM_TWO", 0);
