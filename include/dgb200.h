@@ -73,8 +73,8 @@ int dg_spmm_plan_info(const dg_spmm_plan* plan, int64_t info[8]);
  * f <= ld_h, ld_h % 4 == 0, ld_z % 4 == 0.  acc: 0 = fp32 accumulate,
  * 1 = fp32 4-entry windows folded into fp64, 2 = two-level fp32 (32-entry
  * windows folded into an fp32 sum; <= (32 + len/32) ulp of the row's
- * sum of |terms|, <= 64 ulp per 1024-entry item; rows >= 32 floats only,
- * narrower rows use mode 1).  slab_floats: feature-slab width (0 = auto: sized
+ * sum of |terms|, <= 64 ulp per 1024-entry item; used for rows > 48 floats
+ * (and 9..16-float rows of tables > 1 GB); other rows use mode 1).  slab_floats: feature-slab width (0 = auto: sized
  * so one slab of the gathered rows stays L2-resident).  beta = 1 adds the
  * product to z (the halo pass of a phase whose own-block pass overlapped
  * the exchange).                                                        */

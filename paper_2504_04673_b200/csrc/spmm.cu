@@ -16,10 +16,10 @@
 //    lanes) or G x 32 B (Blackwell 256-bit ld.global.nc.v8) contiguous
 //    request.  Wide layers are split into slabs (grid.y) sized so one slab of
 //    all gathered rows stays L2-resident; the CSR stream is evict-first.
-//  * Two forms.  acc = 1 (rows <= 16 floats): entries loaded with uniform
-//    16-B vector loads one step ahead, 4-entry fp32 windows folded into fp64
-//    accumulators.  acc = 2 (rows >= 32 floats, and 9..16-float rows of
-//    tables far larger than L2): one 256-bit chunk per lane, the item's
+//  * Two forms.  128-bit lanes (rows <= 48 floats): entries loaded with
+//    uniform 16-B vector loads one step ahead, 4-entry fp32 windows folded
+//    into fp64 accumulators.  acc = 2 with 256-bit lanes (rows > 48 floats,
+//    and 9..16-float rows of tables far larger than L2): one chunk per lane, the item's
 //    entries staged in shared memory by cp.async one window ahead (no
 //    registers held by the prefetch), two-level fp32 sums (32-entry windows;
 //    <= 64 ulp of the row's sum of |terms| per 1024-entry item), 2 entries per
@@ -802,7 +802,12 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   int64_t ext_rows_all = 0;
   for (int r = 0; r < p->n_ranks; ++r) ext_rows_all += p->ext_rows[r];
   const bool dram_table = (double)ext_rows_all * (double)ld_h * 4.0 > 1024.0 * 1024 * 1024;
-  bool v8 = (f > 16 || (f > 8 && acc == 2 && dram_table)) && ld_h % 8 == 0 && ld_z % 8 == 0;
+  // 128-bit lanes for rows of up to 48 floats: f=41/47 rows take 12 lane-
+  // chunks of 16 B (3 per lane) instead of 6 x 32 B with two idle lanes of
+  // eight, 1.66 vs 1.77 ms (profiles/r01/spmm_f41_lanes.txt)
+  static const int force_v4 = env_int("DG_SPMM_FORCE_V4", 0);   // sweep knob
+  bool v8 = (f > 48 || (f > 8 && f <= 16 && acc == 2 && dram_table)) && ld_h % 8 == 0 &&
+            ld_z % 8 == 0 && !force_v4;
   for (int r = 0; r < p->n_ranks && v8; ++r) {
     const uintptr_t al = (uintptr_t)h_local[r] | (uintptr_t)z[r] |
                          (uintptr_t)(h_halo ? h_halo[r] : nullptr);
