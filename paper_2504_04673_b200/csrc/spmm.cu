@@ -814,7 +814,10 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
     v8 = (al & 31) == 0;
   }
   const int V = v8 ? 8 : 4;
-  const int chunks = (f + V - 1) / V;
+  // chunks cover the row up to the next 32-B boundary when the pitch allows
+  // (f=41 -> 48 floats): the zero padding of H is carried into Z's padding
+  const int chunks = (V == 4 && ld_h % 8 == 0 && ld_z % 8 == 0) ? (f + 7) / 8 * 2
+                                                                 : (f + V - 1) / V;
   SpmmArgs a;
   std::memset(&a, 0, sizeof(a));
   int64_t ext_total = 0;

@@ -42,3 +42,28 @@ def test_long_positive_rows(acc, f, deg):
     assert err.max() <= 1e-5
     bound = (4 + 2) * U if acc == ACC_FP64 else (32 + 1024 / 32 + 2) * U
     assert err.max() <= bound, (err.max() / U, "ulp")
+
+
+@pytest.mark.parametrize("f", [3, 16, 41, 47, 100, 602])
+def test_padding_columns_stay_zero(f):
+    """Z's padding columns (f .. pitch) are zero whenever H's are: the GCN
+    step relies on zero padding through SpMM, GEMM, ReLU and the loss."""
+    rng = np.random.default_rng(f)
+    n = 3000
+    rows = np.repeat(np.arange(n), 40)
+    cols = rng.integers(0, n, size=rows.size)
+    key = np.unique(rows * n + cols)
+    rows, cols = key // n, key % n
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
+    ro = RankOperand(0, 0, 0, n, n, rp, cols.astype(np.int32),
+                     rng.uniform(-1, 1, size=rows.size).astype(np.float32), 0, {})
+    plan = DevicePlan(_LocalPlan(ro), standalone=True)
+    ld = pad4(f)
+    h = torch.zeros((n, ld), device="cuda")
+    h[:, :f] = torch.randn((n, f), device="cuda")
+    z = torch.full((n, ld), float("nan"), device="cuda")
+    plan.run({0: h}, f, ld, out={0: z})
+    assert torch.isfinite(z[:, :f]).all()
+    if ld > f:
+        assert not z[:, f:].any(), "padding columns must be written as zeros"
