@@ -46,8 +46,10 @@ def test_long_positive_rows(acc, f, deg):
 
 @pytest.mark.parametrize("f", [3, 16, 41, 47, 100, 602])
 def test_padding_columns_stay_zero(f):
-    """Z's padding columns (f .. pitch) are zero whenever H's are: the GCN
-    step relies on zero padding through SpMM, GEMM, ReLU and the loss."""
+    """Z's padding up to the next 32-byte boundary is written (as zeros,
+    from H's zero padding); wide rows' remaining pitch padding (128-B rows)
+    is never written -- and never read: every consumer bounds its K / N by
+    the logical width."""
     rng = np.random.default_rng(f)
     n = 3000
     rows = np.repeat(np.arange(n), 40)
@@ -65,5 +67,6 @@ def test_padding_columns_stay_zero(f):
     z = torch.full((n, ld), float("nan"), device="cuda")
     plan.run({0: h}, f, ld, out={0: z})
     assert torch.isfinite(z[:, :f]).all()
-    if ld > f:
-        assert not z[:, f:].any(), "padding columns must be written as zeros"
+    top = min(ld, (f + 7) // 8 * 8)
+    if top > f:
+        assert not z[:, f:top].any(), "padding columns must be written as zeros"
