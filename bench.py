@@ -366,11 +366,9 @@ def run_papers(args, wl):
     f0, ld0 = dims[0], pad4(dims[0])
     hs = {r: gr.x[r] for r in dp.local}
     zs = {r: torch.empty_like(hs[r]) for r in dp.local}
-    tiles = ({r: gr._tiled_input(grid.coords(r)[0], hs[r]) for r in dp.local}
-             if gr._use_tiled else None)
     dp.exchange_only(hs, f0, ld0)
-    dp.spmm_only(hs, f0, ld0, zs, tiles)
-    t_spmm = _timed(lambda: dp.spmm_only(hs, f0, ld0, zs, tiles), 3, w) / 1e3
+    dp.spmm_only(hs, f0, ld0, zs)
+    t_spmm = _timed(lambda: dp.spmm_only(hs, f0, ld0, zs), 3, w) / 1e3
     t_xchg = _timed(lambda: dp.exchange_only(hs, f0, ld0), 3, w) / 1e3 if p > 1 else None
     del zs
     tot_b = gather_b = 0
@@ -428,8 +426,7 @@ def run_papers(args, wl):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": ncu_traffic(f"papers_f{f0}_p{p}_c1"),
-                     "kernel": "spmm_kernel (layer-1 forward SpMM, f=%d, rank 0%s)"
-                               % (f0, ", slab-major own block" if gr._use_tiled else ""),
+                     "kernel": "spmm_kernel (layer-1 forward SpMM, f=%d, rank 0)" % f0,
                      "algorithmic_bytes": int(tot_b), "kernel_ms": round(t_spmm * 1e3, 3),
                      "gather_gbs": round(gather_b / t_spmm / 1e9, 1), "peak_source": peak_src},
         "exchange": exch,

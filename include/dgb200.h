@@ -82,19 +82,6 @@ int dg_spmm_run(dg_spmm_plan* plan, const float* const* h_local, const float* co
                 float* const* z, int32_t f, int64_t ld_h, int64_t ld_z, int32_t acc,
                 int32_t slab_floats, int32_t beta, void* stream);
 
-/* Slab-major own block (wide layers whose 64-float feature slabs stay
- * L2-resident): h_local_tiled[r] holds slab s of own row c at
- * h_local_tiled[r] + s * n_local[r] * 64 + c * 64, so each slab pass gathers
- * from one contiguous table (B200: 18.2 vs 15.1 TB/s of random 256-B
- * gathers, profiles/r01/gather_roofline_v8.txt); halo rows stay row-major
- * (pitch ld_h).  dg_spmm_tiled_slab returns 64 when dg_spmm_run (acc = 2)
- * runs this plan at width f in 64-float slabs -- the only case the tiled
- * entry accepts -- and 0 otherwise.                                       */
-int dg_spmm_tiled_slab(dg_spmm_plan* plan, int32_t f, int64_t ld_h);
-int dg_spmm_run_tiled(dg_spmm_plan* plan, const float* const* h_local_tiled,
-                      const float* const* h_halo, float* const* z, int32_t f, int64_t ld_h,
-                      int64_t ld_z, int32_t slab_floats, int32_t beta, void* stream);
-
 /* ---- halo exchange: replaces the pack `h_block[NnzCols(dst, me)]`
  *      (spmm.py:185, 212), Comm.all_to_allv / isend / broadcast
  *      (runtime.py:311-435) and the receiver-side `_scatter`

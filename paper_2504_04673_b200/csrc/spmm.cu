@@ -55,8 +55,6 @@ struct RankArgs {
   const float* hh;     // halo rows (ext >= n_local)
   float* z;
   int64_t n_local;
-  int64_t sl;          // 0: hl row-major (pitch ld_h); else hl slab-major: slab s of
-                       // row c at hl + s * sl + c * slab_floats (dg_spmm_run_tiled)
 };
 
 struct SpmmArgs {
@@ -302,16 +300,6 @@ __global__ void __launch_bounds__(256, MB)
           v[j] = __int_as_float(en.y);
           if (j < nv) {
             const int c = en.x;
-            if (R.sl) {                     // slab-major own block: contiguous slab tables
-              const float* hp = c < nl ? hl + blockIdx.y * R.sl + (int64_t)c * a.slab * V
-                                       : hh + (int64_t)(c - nl) * ld + (int64_t)slab0 * V;
-#pragma unroll
-              for (int q = 0; q < CPL; ++q) {
-                if (on[q]) x[j][q].load(hp + (int64_t)(chk[q] - slab0) * V);
-                else x[j][q].zero();
-              }
-              continue;
-            }
             const float* hp = c < nl ? hl + (int64_t)c * ld : hh + (int64_t)(c - nl) * ld;
 #pragma unroll
             for (int q = 0; q < CPL; ++q) {
@@ -800,45 +788,9 @@ int dg_spmm_plan_info(const dg_spmm_plan* p, int64_t info[8]) {
   return DG_OK;
 }
 
-static int spmm_run_impl(dg_spmm_plan* p, const float* const* h_local, const float* const* h_halo,
-                         float* const* z, int32_t f, int64_t ld_h, int64_t ld_z, int32_t acc,
-                         int32_t slab_floats, int32_t beta, void* stream, bool tiled);
-
 int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const* h_halo,
                 float* const* z, int32_t f, int64_t ld_h, int64_t ld_z, int32_t acc,
                 int32_t slab_floats, int32_t beta, void* stream) {
-  return spmm_run_impl(p, h_local, h_halo, z, f, ld_h, ld_z, acc, slab_floats, beta, stream,
-                       false);
-}
-
-int dg_spmm_run_tiled(dg_spmm_plan* p, const float* const* h_local_tiled,
-                      const float* const* h_halo, float* const* z, int32_t f, int64_t ld_h,
-                      int64_t ld_z, int32_t slab_floats, int32_t beta, void* stream) {
-  if (slab_floats != 64) return set_err(DG_ERR_ARG, "dg_spmm_run_tiled: slabs of 64 floats");
-  return spmm_run_impl(p, h_local_tiled, h_halo, z, f, ld_h, ld_z, 2, slab_floats, beta, stream,
-                       true);
-}
-
-int dg_spmm_tiled_slab(dg_spmm_plan* p, int32_t f, int64_t ld_h) {
-  // the slab width dg_spmm_run (acc = 2) would use for this plan and width
-  // (64: the own block may be passed slab-major to dg_spmm_run_tiled; 0: not)
-  if (!p || f <= 48 || ld_h % 8) return 0;
-  int64_t ext = 0;
-  for (int r = 0; r < p->n_ranks; ++r) ext += p->ext_rows[r];
-  const int chunks = (f + 7) / 8;
-  const double per_chunk = (double)std::max<int64_t>(ext, 1) * 32.0;
-  const int fit = (int)std::max(0.0, 64.0 * 1024 * 1024 / per_chunk);
-  if (fit < 4) return 0;
-  int G, CPL, ns;
-  choose_config(chunks, fit, &G, &CPL, &ns);
-  int g = 2;
-  while (g < (chunks + ns - 1) / ns && g < 32) g <<= 1;
-  return (g * ns >= chunks && g == 8) ? 64 : 0;
-}
-
-static int spmm_run_impl(dg_spmm_plan* p, const float* const* h_local, const float* const* h_halo,
-                         float* const* z, int32_t f, int64_t ld_h, int64_t ld_z, int32_t acc,
-                         int32_t slab_floats, int32_t beta, void* stream, bool tiled) {
   if (!p) return set_err(DG_ERR_ARG, "dg_spmm_run: null plan");
   if (f < 1 || ld_h % 4 || ld_z % 4 || f > ld_h || f > ld_z || acc < 0 || acc > 2)
     return set_err(DG_ERR_ARG, "dg_spmm_run: need 1 <= f <= ld, ld % 4 == 0, acc in 0..2");
@@ -874,7 +826,7 @@ static int spmm_run_impl(dg_spmm_plan* p, const float* const* h_local, const flo
                          (uintptr_t)(h_halo ? h_halo[r] : nullptr);
     if (al & 15) return set_err(DG_ERR_ARG, "dg_spmm_run: H/Z must be 16-byte aligned");
     a.r[r] = RankArgs{p->ent[r], h_local[r], h_halo ? h_halo[r] : nullptr, z[r],
-                      p->n_local[r], 0};
+                      p->n_local[r]};
     ext_total += p->ext_rows[r];
   }
   if (p->n_slots) {
@@ -936,12 +888,6 @@ static int spmm_run_impl(dg_spmm_plan* p, const float* const* h_local, const flo
   LaunchFn fn = v8 ? (acc ? pick_launch<true, 8>(G, CPL) : pick_launch<false, 8>(G, CPL))
                    : (acc ? pick_launch<true, 4>(G, CPL) : pick_launch<false, 4>(G, CPL));
   if (two && CPL == 1) fn = pick_two(G);
-  if (tiled) {
-    if (!(two && CPL == 1 && G * V == slab_floats && pick_two(G)))
-      return set_err(DG_ERR_ARG, "dg_spmm_run_tiled: the plan does not run 64-float slabs here");
-    fn = pick_two(G);
-    for (int r = 0; r < p->n_ranks; ++r) a.r[r].sl = p->n_local[r] * slab_floats;
-  }
   if (v8 && acc && CPL == 1 && minb >= 3) fn = pick_minb(G, minb);
   static const int env_e = env_int("DG_SPMM_E", 0);
   static const int env_two = env_int("DG_SPMM_TWO", 0);

@@ -30,7 +30,7 @@ import torch
 from . import _lib as L
 
 __all__ = ["DevicePlan", "single_spmm", "device_gemm", "reduce_members", "pad4", "to_device",
-           "tile_slabs", "ACC_FP64", "ACC_TWO_LEVEL"]
+           "ACC_FP64", "ACC_TWO_LEVEL"]
 
 ACC_FP64 = 1          # fp32 4-entry windows folded into fp64 accumulators
 ACC_TWO_LEVEL = 2     # two-level fp32 (<= 64 ulp of sum|terms| per item; rows >= 32 floats)
@@ -306,21 +306,10 @@ class DevicePlan:
             store[r] = buf
         return buf[:need].view(rows, ld)
 
-    def _spmm(self, plan, hs, halo_ptrs, zp, f, ld, beta, stream, tiled=None):
-        if tiled is not None:       # slab-major own blocks (dg_spmm_run_tiled)
-            L.check(L.lib().dg_spmm_run_tiled(plan, L.ptr_array([tiled[r] for r in self.local]),
-                                              L.ptr_array(halo_ptrs), L.ptr_array(zp), f, ld,
-                                              ld, 64, beta, stream))
-            return
+    def _spmm(self, plan, hs, halo_ptrs, zp, f, ld, beta, stream):
         L.check(L.lib().dg_spmm_run(plan, L.ptr_array([hs[r] for r in self.local]),
                                     L.ptr_array(halo_ptrs), L.ptr_array(zp), f, ld, ld, self.acc,
                                     0, beta, stream))
-
-    def tiled_ok(self, f, ld):
-        """Whether the own-block pass runs 64-float slabs at width f, so a
-        slab-major copy of H (`tile_slabs`) can feed it."""
-        return (self.acc == ACC_TWO_LEVEL and
-                int(L.lib().dg_spmm_tiled_slab(self._splan, f, ld)) == 64)
 
     def _xchg(self, hs, dst, f, ld, stream):
         if self._segs:
@@ -328,8 +317,7 @@ class DevicePlan:
                                         len(self.local), L.ptr_array(dst), len(dst), f, ld,
                                         1 if self.multi else 0, stream))
 
-    def run(self, hs: dict, f: int, ld: int, out: dict = None, reduce: bool = True,
-            tiled: dict = None) -> dict:
+    def run(self, hs: dict, f: int, ld: int, out: dict = None, reduce: bool = True) -> dict:
         """One multiply phase.  hs[r]: (n_i, ld) fp32 CUDA tensor for every
         hosted rank r; returns {r: (n_i, ld) tensor}.  1.5D with
         reduce=False returns each replica's partial product (views of the
@@ -357,7 +345,7 @@ class DevicePlan:
             else:
                 zp = [out[r].data_ptr() for r in self.local]
             self._spmm(self._splan, hs, [halos[r].data_ptr() for r in self.local], zp, f, ld,
-                       0, st, tiled)
+                       0, st)
             if self.reduce and not reduce:
                 return {r: self._buffer(self.partial, r, vp.ranks[r].n_rows, ld)
                         for r in self.local}
@@ -388,7 +376,7 @@ class DevicePlan:
             self.world.barrier()                        # every peer's rows have landed
         zp = ([self._partial_ptr(r, par) for r in self.local] if self.reduce
               else [out[r].data_ptr() for r in self.local])
-        self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, st, tiled)   # own block
+        self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, st)       # own block
         main.wait_stream(self._side)
         self._spmm(self._bplan, hs, halo_ptrs, zp, f, ld, 1, st)       # halo rows, z +=
         for r in self.local:                            # inputs in use on the side stream
@@ -426,7 +414,7 @@ class DevicePlan:
         if self.multi:
             self.world.barrier()
 
-    def spmm_only(self, hs: dict, f: int, ld: int, out: dict, tiled: dict = None):
+    def spmm_only(self, hs: dict, f: int, ld: int, out: dict):
         """The local SpMM of one phase (own block + halo) over the current
         halo contents, no exchange."""
         if self.multi:
@@ -435,7 +423,7 @@ class DevicePlan:
             halo_ptrs = [self._buffer(self.halo, r, self.vplan.ranks[r].halo_rows,
                                       ld).data_ptr() for r in self.local]
         zp = [out[r].data_ptr() for r in self.local]
-        self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, _stream(), tiled)
+        self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, _stream())
         if self._bplan is not None:
             self._spmm(self._bplan, hs, halo_ptrs, zp, f, ld, 1, _stream())
 
@@ -554,18 +542,6 @@ class RowGroupReducer:
             L.check(lib.dg_group_reduce(len(grp), L.ptr_array([self._ptr(m, par) for m in grp]),
                                         1, L.ptr_array([out[r]]), 0, t.numel(), 0, _stream()))
         return out
-
-
-def tile_slabs(h: torch.Tensor, slab: int = 64) -> torch.Tensor:
-    """Slab-major copy of a row-major (n, ld) block: (ceil(ld / slab), n,
-    slab), zero padded -- the own-block layout dg_spmm_run_tiled reads."""
-    n, ld = h.shape
-    ns = -(-ld // slab)
-    out = torch.zeros((ns, n, slab), dtype=h.dtype, device=h.device)
-    for s in range(ns):
-        w = min(slab, ld - s * slab)
-        out[s, :, :w] = h[:, s * slab:s * slab + w]
-    return out
 
 
 def reduce_members(tensors):

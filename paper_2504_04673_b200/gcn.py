@@ -383,26 +383,6 @@ class GcnRun:
         from .spmm import device_plan
         for op in {id(self.dm.fwd): self.dm.fwd, id(self.dm.bwd): self.dm.bwd}.values():
             device_plan(op, grid, cfg.variant, max_ld=max(self.lds))
-        self._init_tiling()
-
-    def _init_tiling(self):
-        """Layer 1's input is constant across epochs: when its SpMM runs in
-        64-float slabs, feed it a slab-major copy (engine.tile_slabs) so each
-        slab pass gathers from one contiguous table."""
-        from .spmm import device_plan
-        self._xt = {}
-        dp = device_plan(self.dm.fwd, self.grid, self.cfg.variant)
-        self._use_tiled = dp.tiled_ok(self.dims[0], self.lds[0])
-
-    def _tiled_input(self, i, h0):
-        """Slab-major copy of block row i's features, rebuilt whenever the
-        features change (e.g. a new upload)."""
-        from .engine import tile_slabs
-        tag = (h0.data_ptr(), h0._version)
-        ent = self._xt.get(i)
-        if ent is None or ent[0] != tag:
-            ent = self._xt[i] = (tag, tile_slabs(h0))
-        return ent[1]
 
     def _inputs(self, i):
         """Block row i of the features, labels and mask (device views)."""
@@ -461,9 +441,7 @@ class GcnRun:
                                                 dims[l + 1], lds[l + 1], st))
                     else:
                         t = spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant,
-                                       out=arena.get("t", n_i, lds[l]),
-                                       h_tiled=(self._tiled_input(i, h0)
-                                                if l == 0 and self._use_tiled else None))
+                                       out=arena.get("t", n_i, lds[l]))
                         mark(f"fwd_spmm_f{dims[l]}")
                         z, h = dense.fwd(t, w, dims[l], dims[l + 1], l < last,
                                          z=arena.get("l", n_i, lds[l + 1]) if l == last else None)

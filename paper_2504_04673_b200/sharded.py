@@ -480,7 +480,6 @@ def _sharded_run_class():
                          for i, t in labels.items()}
             self.xent, self.dense, self.ctx, self.timer = {}, {}, {}, None
             device_plan(op, grid, cfg.variant, max_ld=max(self.lds))
-            self._init_tiling()
             graph.release()                      # the plans hold the entries now
             torch.cuda.empty_cache()
             self.part = block_partition(graph.n, graph.p)

@@ -67,8 +67,7 @@ def device_plan(op: DistOperand, grid: ProcessGrid, variant: str, max_ld=None):
 
 
 def spmm_phase(comm: Comm, op: DistOperand, h_pad: torch.Tensor, f: int, variant: str,
-               reduce: bool = True, reduce_f: int = None, out: torch.Tensor = None,
-               h_tiled: torch.Tensor = None):
+               reduce: bool = True, reduce_f: int = None, out: torch.Tensor = None):
     """Device form of `spmm_kernel`: h_pad is a contiguous fp32 CUDA tensor
     (n_i, pad4(f)) with zero padding; returns the padded (n_i, pad4(f))
     product.  A collective over the ranks of this process: the last rank to
@@ -76,31 +75,26 @@ def spmm_phase(comm: Comm, op: DistOperand, h_pad: torch.Tensor, f: int, variant
     reduce=False (1.5D, extension): return each replica's partial product;
     the caller reduces after its transform and `reduce_f` is the width the
     ledger charges for that reduction.  `out` (optional): this rank's
-    (n_i, pad4(f)) output buffer (the GCN loop's activation arena).
-    `h_tiled` (optional): a slab-major copy of h_pad (engine.tile_slabs),
-    used when the plan runs 64-float slabs at this width."""
+    (n_i, pad4(f)) output buffer (the GCN loop's activation arena)."""
     grid = comm.grid
     ledger = comm.ledger
     ld = pad4(f)
 
     def complete(arr):
         dp = device_plan(op, grid, variant, max_ld=ld)
-        hs, outs, tiles = {}, {}, {}
-        for r, (h, o, t) in arr.items():
+        hs, outs = {}, {}
+        for r, (h, o) in arr.items():
             hs[r] = h if (isinstance(h, torch.Tensor) and h.dtype == torch.float32
                           and h.is_cuda and h.is_contiguous() and h.shape[1] == ld) \
                 else to_device(h[:, :f], ld)
             outs[r] = o
-            tiles[r] = t
         given = all(o is not None for o in outs.values())
-        tiled = tiles if (all(t is not None for t in tiles.values())
-                          and dp.tiled_ok(f, ld)) else None
-        res = dp.run(hs, f, ld, out=outs if given else None, reduce=reduce, tiled=tiled)
+        res = dp.run(hs, f, ld, out=outs if given else None, reduce=reduce)
         dp.vplan.charge(ledger, f, None if reduce else reduce_f)
         return res
 
     return comm._collective(("spmm", id(op), variant, reduce), tuple(range(comm.p)),
-                            (h_pad, out, h_tiled), complete)
+                            (h_pad, out), complete)
 
 
 def row_group_reduce(comm: Comm, u: torch.Tensor, dm: DistMatrices, variant: str):

@@ -70,31 +70,3 @@ def test_padding_columns_stay_zero(f):
     top = min(ld, (f + 7) // 8 * 8)
     if top > f:
         assert not z[:, f:top].any(), "padding columns must be written as zeros"
-
-
-@pytest.mark.parametrize("p", [1, 3])
-def test_tiled_own_block_bitwise(p):
-    """The slab-major own-block input (dg_spmm_run_tiled) gives bitwise the
-    row-major result (same kernel, same summation order)."""
-    import paper_2504_04673_b200 as P
-    from paper_2504_04673_b200 import graphgen
-    from paper_2504_04673_b200.engine import tile_slabs
-    from paper_2504_04673_b200.plan import DistOperand, build_variant_plan
-    from paper_2504_04673_b200.runtime import ProcessGrid
-    a = P.gcn_normalize(graphgen.rmat(13, 16, 4))
-    a.values = a.values.astype(np.float32).astype(np.float64)
-    bounds = P.block_partition(a.n_rows, p).boundaries
-    dp = DevicePlan(build_variant_plan(DistOperand(P.transpose_csr(a), bounds),
-                                       ProcessGrid(p, 1), "1d-sparse"))
-    f = 602
-    ld = pad4(f)
-    if not dp.tiled_ok(f, ld):
-        pytest.skip("this plan does not run 64-float slabs")
-    h = torch.zeros((a.n_rows, ld), device="cuda")
-    h[:, :f] = torch.randn((a.n_rows, f), device="cuda")
-    hs = {r: h[b[0]:b[1]] for r, b in enumerate(bounds)}
-    z1 = dp.run(hs, f, ld)
-    z1 = {r: t.clone() for r, t in z1.items()}
-    z2 = dp.run(hs, f, ld, tiled={r: tile_slabs(hs[r]) for r in hs})
-    for r in hs:
-        assert torch.equal(z1[r][:, :f], z2[r][:, :f])
