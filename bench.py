@@ -87,6 +87,22 @@ def nvlink_peak():
         return 770.0, "B200_PROFILING.md measured peer copy"
 
 
+def gather_probe(rows, ld):
+    """Measured pure-gather rate (random 256-B row slabs, 256-bit loads, no
+    CSR, no math) for this table geometry, from profiles/r01/
+    gather_roofline_v8.txt (scripts/gather_roofline.py), or None."""
+    import re
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "gather_roofline_v8.txt")) as fh:
+            for line in fh:
+                m = re.match(r"rows=(\d+) ld=(\d+) row_bytes=256 v8=True .*: (\d+) GB/s", line)
+                if m and int(m.group(1)) == rows and int(m.group(2)) == ld:
+                    return float(m.group(3))
+    except OSError:
+        pass
+    return None
+
+
 def peaks():
     try:
         with open(PEAKS) as fh:
@@ -549,6 +565,7 @@ def run_ours(args, wl):
         gather_b += 4 * (m + 1) + 8 * nnz + 4 * f0 * nnz + 4 * f0 * m
     peak, peak_src = peaks()
     achieved = tot_b / t_spmm / 1e9
+    probe = gather_probe(n, ld0) if p == 1 else None
 
     # ---- all SpMM phases of one epoch (HBM GB/s over the epoch's SpMMs) --
     widths = dims[:-1] + dims[1:]
@@ -646,7 +663,10 @@ def run_ours(args, wl):
                      "traffic": ncu_traffic(f"{args.workload}_f{f0}_p{p}_c{c}"),
                      "kernel": "spmm_kernel (layer-1 forward SpMM, f=%d, rank 0)" % f0,
                      "algorithmic_bytes": int(tot_b), "kernel_ms": round(t_spmm * 1e3, 3),
-                     "gather_gbs": round(gather_b / t_spmm / 1e9, 1), "peak_source": peak_src},
+                     "gather_gbs": round(gather_b / t_spmm / 1e9, 1), "peak_source": peak_src,
+                     "gather_probe_gbs": probe,
+                     "gather_frac_of_probe": (round(gather_b / t_spmm / 1e9 / probe, 3)
+                                              if probe else None)},
         "exchange": exch,
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h[0] // e2e_steps)},
