@@ -628,8 +628,10 @@ def run_ours(args, wl):
             copy_stream.wait_stream(torch.cuda.current_stream())
             state["ev"] = upload(xbuf[(k + 1) % 2], copy_stream)
         gr.x = cur
-        rr = gr.run(1)       # eager: the graph's input buffer is fixed, the upload alternates
-        st = rr.results[grid.rank_of(0, 0)]["stats"].cpu()   # loss / correct to host
+        # eager (the graph's input buffer is fixed, the upload alternates);
+        # the step's loss: a device-side sum over every rank, then 16 B to host
+        rr = gr.run(1, gather=False)
+        st = gr.global_stats(rr).cpu()
         d2h[0] += st.numel() * st.element_size()
         state["k"] = k + 1
 

@@ -470,7 +470,10 @@ class GcnRun:
                 comm.ledger_mark(("epoch", epoch))
         return {"stats": stats, "weights": ws}
 
-    def run(self, epochs=None):
+    def run(self, epochs=None, gather=True):
+        """`epochs` training epochs.  gather=False (multi-process): skip the
+        end-of-run host gather of every rank's results; pair with
+        `global_stats` to read the loss (a device-side sum over all ranks)."""
         epochs = self.cfg.epochs if epochs is None else epochs
         p = self.grid.p
         from .dist import world
@@ -480,7 +483,34 @@ class GcnRun:
                  for r in hosted}
         return run_program(p, self.grid.c,
                            lambda comm: self.program(comm, epochs, stats[comm.rank]),
-                           ctx=self.ctx)
+                           ctx=self.ctx, gather=gather)
+
+    def global_stats(self, run):
+        """(loss sum, correct) per epoch summed over every rank, as a device
+        tensor on this process: one device reduction over the row groups'
+        first replicas (their rows partition the vertices), no host gather.
+        Collective under torchrun."""
+        from .dist import world
+        w = world()
+        grid = self.grid
+        firsts = tuple(grid.rank_of(i, 0) for i in range(grid.n_rows))
+        if not w.multi:
+            tot = run.results[firsts[0]]["stats"].clone()
+            for r in firsts[1:]:
+                tot += run.results[r]["stats"]
+            return tot
+        hosted = w.local_ranks(grid.p)
+        st = {r: run.results[r]["stats"].float() for r in hosted}
+        # members outside the first replicas contribute zeros
+        st = {r: (t if r in firsts else torch.zeros_like(t)) for r, t in st.items()}
+        numel = next(iter(st.values())).numel()
+        key = ("stats_reducer", numel)
+        red = self.ctx.get(key)
+        if red is None:
+            from .engine import GroupReducer
+            red = self.ctx[key] = GroupReducer(grid.p, numel)
+        out = red(st, {r: tuple(range(grid.p)) for r in hosted})
+        return out[hosted[0]].double()
 
     def run_graph(self, epochs=None):
         """`run` with the epoch captured once in a CUDA graph and replayed

@@ -124,6 +124,22 @@ def main():
         n_checked += 1
         del x, y, sg
         torch.cuda.empty_cache()
+    # gather-free runs: the device-side global loss equals the gathered one
+    from paper_2504_04673_b200.gcn import GcnRun
+    a = P.gcn_normalize(graphgen.rmat(10, 8, 6))
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((a.n_rows, 20)).astype(np.float32)
+    yv = rng.integers(0, 6, a.n_rows)
+    cfg = P.TrainConfig(layers=3, hidden=16, lr=0.1, epochs=2, seed=3)
+    for p in sorted({w.size, 2 * w.size}):
+        gr = GcnRun(a, x, yv, np.ones(a.n_rows, bool), cfg, p=p)
+        full = gr.result(gr.run())
+        tot = gr.global_stats(gr.run(gather=False)).cpu().numpy()
+        losses = tot[:, 0] / a.n_rows
+        if not np.allclose(losses, full.losses, rtol=1e-6, atol=0):
+            fails.append(("global_stats", p, losses.tolist(), full.losses.tolist()))
+        gr.close()
+        n_checked += 1
     print(f"[proc {w.proc}/{w.size}] checked {n_checked} cases, {len(fails)} failures",
           flush=True)
     for f in fails:
