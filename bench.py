@@ -229,6 +229,25 @@ def cpu_reference_epoch_ms(a_hat, wl, budget_s=20.0, nnz_total=None):
     return ms, {f: r for f, r in rates.items()}, sample
 
 
+def host_info():
+    """The CPU the reference arm ran on (nproc, model, RAM)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    info["cpu"] = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemTotal"):
+                    info["ram_gb"] = round(int(line.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    return info
+
+
 def run_reference(args, wl):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -250,7 +269,7 @@ def run_reference(args, wl):
         "config": {"workload": wl["desc"], "variant": args.variant,
                    "p": args.gpus * args.ranks_per_gpu, "c": args.c},
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": 1, "kind": "port",
-                         "sample": sample,
+                         "sample": sample, "host": host_info(),
                          "rates_nnz_f_per_s": {str(k): round(v) for k, v in rates.items()}},
         "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -644,7 +663,7 @@ def run_ours(args, wl):
     if lead and args.gpus == 1 and not args.no_cpu_baseline:
         cms, rates, sample = cpu_reference_epoch_ms(a_hat, wl, budget_s=args.ref_budget)
         cpu = {"value": round(cms, 1), "unit": "ms", "cores": 1, "kind": "port",
-               "sample": sample}
+               "sample": sample, "host": host_info()}
     if not lead:
         return 0
     line = {
