@@ -530,7 +530,10 @@ def run_ours(args, wl):
     # single process, single rank: the epoch is captured once in a CUDA graph
     # and replayed (same kernels on the same buffers; GcnRun.run_graph)
     use_graph = (args.graph == "on" or (args.graph == "auto" and not w.multi and p == 1))
-    run_epochs = gr.run_graph if use_graph else gr.run
+    # several ranks in one process: one host thread drives them in lock step
+    lockstep = (not w.multi and p > 1 and not args.reduce_after_transform)
+    eager = gr.run_lockstep if lockstep else gr.run
+    run_epochs = gr.run_graph if use_graph else eager
     gr.run(args.warmup)
     if use_graph:
         gr.run_graph(1)                                # capture outside the timed region
@@ -563,7 +566,7 @@ def run_ours(args, wl):
     # ---- per-phase breakdown of one extra epoch (CUDA events between steps)
     from paper_2504_04673_b200.gcn import PhaseTimer
     gr.timer = PhaseTimer()
-    gr.run(1)
+    eager(1)
     breakdown = {k: round(v, 3) for k, v in gr.timer.summary().items()}
     gr.timer = None
 
@@ -649,7 +652,7 @@ def run_ours(args, wl):
         gr.x = cur
         # eager (the graph's input buffer is fixed, the upload alternates);
         # the step's loss: a device-side sum over every rank, then 16 B to host
-        rr = gr.run(1, gather=False)
+        rr = gr.run_lockstep(1) if lockstep else gr.run(1, gather=False)
         st = gr.global_stats(rr).cpu()
         d2h[0] += st.numel() * st.element_size()
         state["k"] = k + 1
@@ -694,6 +697,7 @@ def run_ours(args, wl):
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
         "cuda_graph": bool(use_graph),
+        "host_driver": "lockstep" if lockstep else ("graph" if use_graph else "rank threads"),
         "epoch_breakdown_ms": breakdown,
         "extension_transform_first": None if tf_ms is None else {
             "epoch_ms": round(tf_ms, 3),

@@ -485,6 +485,101 @@ class GcnRun:
                            lambda comm: self.program(comm, epochs, stats[comm.rank]),
                            ctx=self.ctx, gather=gather)
 
+    def run_lockstep(self, epochs=None):
+        """`run` for a single process hosting every rank, driven by one host
+        thread in lock step instead of one thread per rank: each multiply
+        phase is one batched device call for all ranks and the collectives
+        need no rendezvous (the thread-per-rank runtime costs ~60 us per
+        collective and a GIL hand-off per launch at 4 hosted ranks).  Same
+        kernels, same order per rank, same ledger (the reference's
+        conventions); aggregate-first order only.  Results equal `run` bit
+        for bit (tests/test_gpu_api.py)."""
+        from .dist import world
+        from .engine import reduce_members
+        from .plan import index_setup_charges
+        from .runtime import CommLedger, RunResult
+        from .spmm import device_plan
+        epochs = self.cfg.epochs if epochs is None else epochs
+        cfg, dm, grid = self.cfg, self.dm, self.grid
+        if world().multi or cfg.order != "aggregate-first" or cfg.reduce_after_transform:
+            raise ValueError("run_lockstep: single process, aggregate-first order only")
+        p = grid.p
+        ranks = list(range(p))
+        ledger = CommLedger(p)
+        index_setup_charges(ledger, dm.fwd, grid, cfg.variant)
+        if dm.bwd is not dm.fwd:
+            index_setup_charges(ledger, dm.bwd, grid, cfg.variant)
+        dims, lds = self.dims, self.lds
+        last = len(self.w0) - 1
+        lib = L.lib()
+        st = L.stream_ptr()
+        if not hasattr(self, "arena"):
+            self.arena = {}
+        blk, n_i, xent, dense, arena, ws, stats = {}, {}, {}, {}, {}, {}, {}
+        for r in ranks:
+            i, _ = grid.coords(r)
+            r0, r1 = dm.boundaries[i]
+            blk[r] = self._inputs(i)
+            n_i[r] = r1 - r0
+            xent[r] = self.xent.setdefault(r, _Xent(r1 - r0, self.device))
+            dense[r] = self.dense.setdefault(r, _Dense(self.device))
+            arena[r] = self.arena.setdefault(r, _Arena(self.device))
+            ws[r] = [w.clone() for w in self.w0]
+            stats[r] = torch.zeros((max(epochs, 1), 2), dtype=torch.float64, device=self.device)
+        fwd = device_plan(dm.fwd, grid, cfg.variant, max_ld=max(lds))
+        bwd = device_plan(dm.bwd, grid, cfg.variant, max_ld=max(lds))
+        tm = self.timer
+        mark = tm.mark if tm is not None else (lambda name: None)
+        with _no_tf32():
+            for epoch in range(epochs):
+                mark("epoch_start")
+                hs = {r: [blk[r][0]] for r in ranks}
+                zs = {r: [] for r in ranks}
+                for l in range(last + 1):
+                    t = fwd.run({r: hs[r][-1] for r in ranks}, dims[l], lds[l],
+                                out={r: arena[r].get("t", n_i[r], lds[l]) for r in ranks})
+                    fwd.vplan.charge(ledger, dims[l])
+                    mark(f"fwd_spmm_f{dims[l]}")
+                    for r in ranks:
+                        z, h = dense[r].fwd(t[r], ws[r][l], dims[l], dims[l + 1], l < last,
+                                            z=(arena[r].get("l", n_i[r], lds[l + 1])
+                                               if l == last else None))
+                        zs[r].append(z)
+                        hs[r].append(h if l < last else z)
+                    mark(f"fwd_dense_{l}")
+                g = {}
+                for r in ranks:
+                    logits = hs[r][-1]
+                    g[r] = arena[r].get("g", logits.shape[0], logits.shape[1])
+                    xent[r](logits, dims[-1], blk[r][1], blk[r][2], self.denom, g[r],
+                            stats[r][epoch])
+                    hs[r][-1] = zs[r][-1] = None
+                mark("xent")
+                for l in range(last, -1, -1):
+                    m = bwd.run(g, dims[l + 1], lds[l + 1],
+                                out={r: arena[r].get("l", n_i[r], lds[l + 1]) for r in ranks})
+                    bwd.vplan.charge(ledger, dims[l + 1])
+                    mark(f"bwd_spmm_f{dims[l + 1]}")
+                    ys = {r: dense[r].wgrad(hs[r][l], m[r], dims[l], dims[l + 1], lds[l],
+                                            lds[l + 1]) for r in ranks}
+                    y = {}
+                    for j in range(grid.c):             # all_reduce_sum over each column group
+                        grp = grid.col_group(j)
+                        for r, o in zip(grp, reduce_members([ys[r] for r in grp])):
+                            y[r] = o
+                        ledger.allreduce(grp, dims[l] * dims[l + 1])
+                    mark(f"bwd_wgrad_{l}")
+                    for r in ranks:
+                        if l > 0:
+                            g[r] = dense[r].bwd(m[r], ws[r][l], dims[l], dims[l + 1],
+                                                zs[r][l - 1])
+                        L.check(lib.dg_sgd(ws[r][l].data_ptr(), y[r].data_ptr(),
+                                           ws[r][l].numel(), float(cfg.lr), st))
+                    mark(f"bwd_dense_{l}")
+                ledger.marks[("epoch", epoch)] = ledger.snapshot()
+        results = [{"stats": stats[r], "weights": ws[r]} for r in ranks]
+        return RunResult(results, ledger, grid)
+
     def global_stats(self, run):
         """(loss sum, correct) per epoch summed over every rank, as a device
         tensor on this process: one device reduction over the row groups'

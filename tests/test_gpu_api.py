@@ -123,3 +123,31 @@ def test_run_graph_equals_eager_run():
             assert np.array_equal(w1, w2)
         assert got.history == ref.history
     gr.close()
+
+
+@pytest.mark.parametrize("p,c,variant", [(4, 1, "1d-sparse"), (4, 2, "15d-sparse"),
+                                         (3, 1, "1d-oblivious")])
+def test_run_lockstep_equals_threaded_run(p, c, variant):
+    """One host thread driving every hosted rank in lock step gives the
+    thread-per-rank runtime's results bit for bit, ledger included."""
+    from paper_2504_04673_b200 import graphgen
+    from paper_2504_04673_b200.gcn import GcnRun
+    a = P.gcn_normalize(graphgen.rmat(10, 8, 4))
+    a.values = a.values.astype(np.float32).astype(np.float64)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((a.n_rows, 20)).astype(np.float32)
+    y = rng.integers(0, 7, a.n_rows)
+    cfg = P.TrainConfig(layers=4, hidden=16, lr=0.1, epochs=3, seed=2, variant=variant)
+    gr = GcnRun(a, x, y, np.ones(a.n_rows, bool), cfg, p=p, c=c)
+    ref = gr.result(gr.run())
+    got = gr.result(gr.run_lockstep())
+    gr.close()
+    assert np.array_equal(got.losses, ref.losses)
+    for w1, w2 in zip(got.weights_per_rank, ref.weights_per_rank):
+        for a1, a2 in zip(w1, w2):
+            assert np.array_equal(a1, a2)
+    assert got.history == ref.history
+    for prim in ref.ledger.counters:
+        for name, v in ref.ledger.counters[prim].items():
+            assert np.array_equal(got.ledger.counters[prim][name], v), (prim, name)
+    assert got.ledger.pair_max_bytes == ref.ledger.pair_max_bytes
