@@ -531,7 +531,7 @@ def run_ours(args, wl):
     # and replayed (same kernels on the same buffers; GcnRun.run_graph)
     use_graph = (args.graph == "on" or (args.graph == "auto" and not w.multi and p == 1))
     # several ranks in one process: one host thread drives them in lock step
-    lockstep = (not w.multi and p > 1 and not args.reduce_after_transform)
+    lockstep = (p > w.size and not args.reduce_after_transform)
     eager = gr.run_lockstep if lockstep else gr.run
     run_epochs = gr.run_graph if use_graph else eager
     gr.run(args.warmup)
@@ -652,7 +652,7 @@ def run_ours(args, wl):
         gr.x = cur
         # eager (the graph's input buffer is fixed, the upload alternates);
         # the step's loss: a device-side sum over every rank, then 16 B to host
-        rr = gr.run_lockstep(1) if lockstep else gr.run(1, gather=False)
+        rr = gr.run_lockstep(1, gather=False) if lockstep else gr.run(1, gather=False)
         st = gr.global_stats(rr).cpu()
         d2h[0] += st.numel() * st.element_size()
         state["k"] = k + 1

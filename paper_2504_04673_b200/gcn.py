@@ -485,27 +485,28 @@ class GcnRun:
                            lambda comm: self.program(comm, epochs, stats[comm.rank]),
                            ctx=self.ctx, gather=gather)
 
-    def run_lockstep(self, epochs=None):
-        """`run` for a single process hosting every rank, driven by one host
-        thread in lock step instead of one thread per rank: each multiply
-        phase is one batched device call for all ranks and the collectives
-        need no rendezvous (the thread-per-rank runtime costs ~60 us per
+    def run_lockstep(self, epochs=None, gather=True):
+        """`run` with this process's ranks driven by one host thread in lock
+        step instead of one thread per rank: each multiply phase is one
+        batched device call for all hosted ranks and the collectives need no
+        host rendezvous (the thread-per-rank runtime costs ~60 us per
         collective and a GIL hand-off per launch at 4 hosted ranks).  Same
         kernels, same order per rank, same ledger (the reference's
         conventions); aggregate-first order only.  Results equal `run` bit
         for bit (tests/test_gpu_api.py)."""
         from .dist import world
-        from .engine import reduce_members
+        from .engine import GroupReducer, reduce_members
         from .plan import index_setup_charges
-        from .runtime import CommLedger, RunResult
+        from .runtime import CommLedger, RunResult, _to_host
         from .spmm import device_plan
         epochs = self.cfg.epochs if epochs is None else epochs
         cfg, dm, grid = self.cfg, self.dm, self.grid
-        if world().multi or cfg.order != "aggregate-first" or cfg.reduce_after_transform:
-            raise ValueError("run_lockstep: single process, aggregate-first order only")
+        if cfg.order != "aggregate-first" or cfg.reduce_after_transform:
+            raise ValueError("run_lockstep: aggregate-first order only")
+        w = world()
         p = grid.p
-        ranks = list(range(p))
-        ledger = CommLedger(p)
+        ranks = w.local_ranks(p) if w.multi else list(range(p))
+        ledger = CommLedger(p, hosted=ranks if w.multi else None)
         index_setup_charges(ledger, dm.fwd, grid, cfg.variant)
         if dm.bwd is not dm.fwd:
             index_setup_charges(ledger, dm.bwd, grid, cfg.variant)
@@ -563,11 +564,22 @@ class GcnRun:
                     ys = {r: dense[r].wgrad(hs[r][l], m[r], dims[l], dims[l + 1], lds[l],
                                             lds[l + 1]) for r in ranks}
                     y = {}
-                    for j in range(grid.c):             # all_reduce_sum over each column group
-                        grp = grid.col_group(j)
-                        for r, o in zip(grp, reduce_members([ys[r] for r in grp])):
-                            y[r] = o
-                        ledger.allreduce(grp, dims[l] * dims[l + 1])
+                    elems = dims[l] * dims[l + 1]
+                    if w.multi:                         # peer-memory group reduction
+                        numel = ys[ranks[0]].numel()
+                        red = self.ctx.get(("reducer", numel))
+                        if red is None:
+                            red = self.ctx[("reducer", numel)] = GroupReducer(p, numel)
+                        groups = {r: grid.col_group(grid.coords(r)[1]) for r in ranks}
+                        y = red(ys, groups)
+                        for grp in sorted(set(groups.values())):
+                            ledger.allreduce(grp, elems)
+                    else:
+                        for j in range(grid.c):         # all_reduce_sum over each column group
+                            grp = grid.col_group(j)
+                            for r, o in zip(grp, reduce_members([ys[r] for r in grp])):
+                                y[r] = o
+                            ledger.allreduce(grp, elems)
                     mark(f"bwd_wgrad_{l}")
                     for r in ranks:
                         if l > 0:
@@ -577,7 +589,17 @@ class GcnRun:
                                            ws[r][l].numel(), float(cfg.lr), st))
                     mark(f"bwd_dense_{l}")
                 ledger.marks[("epoch", epoch)] = ledger.snapshot()
-        results = [{"stats": stats[r], "weights": ws[r]} for r in ranks]
+        results = [None] * p
+        for r in ranks:
+            results[r] = {"stats": stats[r], "weights": ws[r]}
+        if w.multi and gather:                          # as run_program does
+            torch.cuda.synchronize()
+            w.check()
+            parts = w.all_gather_object((_to_host({r: results[r] for r in ranks}), ledger))
+            for res, _ in parts:
+                for r, v in res.items():
+                    results[r] = v
+            ledger = CommLedger.merged([lg for _, lg in parts])
         return RunResult(results, ledger, grid)
 
     def global_stats(self, run):

@@ -140,6 +140,26 @@ def main():
             fails.append(("global_stats", p, losses.tolist(), full.losses.tolist()))
         gr.close()
         n_checked += 1
+    # lock-step host driver (several ranks per process) == thread-per-rank runtime
+    for p, c, variant in [(2 * w.size, 1, "1d-sparse"), (4 * w.size, 2, "15d-sparse")]:
+        if variant.startswith("15d") and p % (c * c):
+            continue
+        cfg = P.TrainConfig(layers=3, hidden=16, lr=0.1, epochs=2, seed=3, variant=variant)
+        gr = GcnRun(a, x, yv, np.ones(a.n_rows, bool), cfg, p=p, c=c)
+        ref = gr.result(gr.run())
+        got = gr.result(gr.run_lockstep())
+        if not np.array_equal(got.losses, ref.losses):
+            fails.append(("lockstep", p, c, got.losses.tolist(), ref.losses.tolist()))
+        for w1, w2 in zip(got.weights_per_rank, ref.weights_per_rank):
+            for a1, a2 in zip(w1, w2):
+                if not np.array_equal(a1, a2):
+                    fails.append(("lockstep weights", p, c))
+        for prim in ref.ledger.counters:
+            for name, v in ref.ledger.counters[prim].items():
+                if not np.array_equal(got.ledger.counters[prim][name], v):
+                    fails.append(("lockstep ledger", p, c, prim, name))
+        gr.close()
+        n_checked += 1
     print(f"[proc {w.proc}/{w.size}] checked {n_checked} cases, {len(fails)} failures",
           flush=True)
     for f in fails:
