@@ -529,7 +529,8 @@ def run_ours(args, wl):
     #      563 MB > 126 MB L2, so no explicit flush is needed) -------------
     # single process, single rank: the epoch is captured once in a CUDA graph
     # and replayed (same kernels on the same buffers; GcnRun.run_graph)
-    use_graph = (args.graph == "on" or (args.graph == "auto" and not w.multi and p == 1))
+    use_graph = (args.graph == "on" or (args.graph == "auto" and not w.multi
+                                          and not args.reduce_after_transform))
     # several ranks in one process: one host thread drives them in lock step
     lockstep = (p > w.size and not args.reduce_after_transform)
     eager = gr.run_lockstep if lockstep else gr.run

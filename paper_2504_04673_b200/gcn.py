@@ -485,7 +485,7 @@ class GcnRun:
                            lambda comm: self.program(comm, epochs, stats[comm.rank]),
                            ctx=self.ctx, gather=gather)
 
-    def run_lockstep(self, epochs=None, gather=True):
+    def run_lockstep(self, epochs=None, gather=True, weights_out=None, stats_out=None):
         """`run` with this process's ranks driven by one host thread in lock
         step instead of one thread per rank: each multiply phase is one
         batched device call for all hosted ranks and the collectives need no
@@ -525,8 +525,9 @@ class GcnRun:
             xent[r] = self.xent.setdefault(r, _Xent(r1 - r0, self.device))
             dense[r] = self.dense.setdefault(r, _Dense(self.device))
             arena[r] = self.arena.setdefault(r, _Arena(self.device))
-            ws[r] = [w.clone() for w in self.w0]
-            stats[r] = torch.zeros((max(epochs, 1), 2), dtype=torch.float64, device=self.device)
+            ws[r] = ([w.clone() for w in self.w0] if weights_out is None else weights_out[r])
+            stats[r] = (torch.zeros((max(epochs, 1), 2), dtype=torch.float64, device=self.device)
+                        if stats_out is None else stats_out[r])
         fwd = device_plan(dm.fwd, grid, cfg.variant, max_ld=max(lds))
         bwd = device_plan(dm.bwd, grid, cfg.variant, max_ld=max(lds))
         tm = self.timer
@@ -632,42 +633,57 @@ class GcnRun:
     def run_graph(self, epochs=None):
         """`run` with the epoch captured once in a CUDA graph and replayed
         (launch-bound small graphs, e.g. config 1).  Single
-        process, one rank, aggregate-first order.  The replayed epochs run
-        exactly the captured kernels on fixed buffers (inputs, activation
-        arena, weights updated in place); the ledger -- host bookkeeping --
-        is extended by the captured epoch's charges once per replay, so the
-        result equals `run` bit for bit (tests/test_gpu_api.py)."""
+        process (one rank, or several driven in lock step), aggregate-first
+        order.  The replayed epochs run exactly the captured kernels on fixed
+        buffers (inputs, activation arena, weights updated in place); the
+        ledger -- host bookkeeping -- is extended by the captured epoch's
+        charges once per replay, so the result equals `run` bit for bit
+        (tests/test_gpu_api.py)."""
         import copy
         from .dist import world
         epochs = self.cfg.epochs if epochs is None else epochs
-        if world().multi or self.grid.p != 1 or self.cfg.order != "aggregate-first":
-            raise ValueError("run_graph: single-process, single-rank, aggregate-first runs only")
+        if world().multi or self.cfg.order != "aggregate-first" or \
+                self.cfg.reduce_after_transform:
+            raise ValueError("run_graph: single-process, aggregate-first runs only")
         dev = self.device
+        p = self.grid.p
         if getattr(self, "_graph", None) is None:
-            self._gw = [w.clone() for w in self.w0]
-            self._gstats = torch.zeros((1, 2), dtype=torch.float64, device=dev)
-            prog = lambda comm: self.program(comm, 1, self._gstats, weights_out=self._gw)  # noqa
-            run_program(1, 1, prog, ctx=self.ctx)          # warm-up: plans, arena, workspaces
+            self._gw = {r: [w.clone() for w in self.w0] for r in range(p)}
+            self._gstats = {r: torch.zeros((1, 2), dtype=torch.float64, device=dev)
+                            for r in range(p)}
+            if p == 1:
+                prog = lambda comm: self.program(comm, 1, self._gstats[0],  # noqa: E731
+                                                 weights_out=self._gw[0])
+                epoch = lambda: run_program(1, 1, prog, ctx=self.ctx)  # noqa: E731
+                base = run_program(1, 1, lambda comm: self.program(comm, 0, self._gstats[0]),
+                                   ctx=self.ctx).ledger
+            else:
+                epoch = lambda: self.run_lockstep(1, weights_out=self._gw,  # noqa: E731
+                                                  stats_out=self._gstats)
+                base = self.run_lockstep(0).ledger          # index setup only
+            epoch()                                        # warm-up: plans, arena, workspaces
             torch.cuda.synchronize()
-            base = run_program(1, 1, lambda comm: self.program(comm, 0, self._gstats),
-                               ctx=self.ctx).ledger       # index setup only
             g = torch.cuda.CUDAGraph()
             side = torch.cuda.Stream(device=dev)
             side.wait_stream(torch.cuda.current_stream())
             n0 = L.launch_count()
             with torch.cuda.stream(side), torch.cuda.graph(g):
-                one = run_program(1, 1, prog, ctx=self.ctx).ledger
+                one = epoch().ledger
             self._graph_launches = L.launch_count() - n0   # our kernels in one epoch
             torch.cuda.current_stream().wait_stream(side)
             torch.cuda.synchronize()
             self._graph, self._gbase, self._gone = g, base, one
-        for w, w0 in zip(self._gw, self.w0):
-            w.copy_(w0)
-        stats = torch.zeros((max(epochs, 1), 2), dtype=torch.float64, device=dev)
+        for r in range(p):
+            for w, w0 in zip(self._gw[r], self.w0):
+                w.copy_(w0)
+        stats = {r: torch.zeros((max(epochs, 1), 2), dtype=torch.float64, device=dev)
+                 for r in range(p)}
         for e in range(epochs):
-            self._gstats.zero_()                          # the loss kernel accumulates
+            for r in range(p):
+                self._gstats[r].zero_()                   # the loss kernel accumulates
             self._graph.replay()
-            stats[e].copy_(self._gstats[0])
+            for r in range(p):
+                stats[r][e].copy_(self._gstats[r][0])
         # ledger: index setup + epochs x the captured epoch's charges
         led = copy.deepcopy(self._gbase)
         base, one = self._gbase, self._gone
@@ -680,8 +696,8 @@ class GcnRun:
         led.pair_max_bytes = dict(one.pair_max_bytes)
         led.pair_max_data_bytes = dict(one.pair_max_data_bytes)
         from .runtime import RunResult
-        return RunResult([{"stats": stats, "weights": [w.clone() for w in self._gw]}], led,
-                         self.grid)
+        return RunResult([{"stats": stats[r], "weights": [w.clone() for w in self._gw[r]]}
+                          for r in range(p)], led, self.grid)
 
     def close(self):
         """Release the run's device state (collective under torchrun)."""

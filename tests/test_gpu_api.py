@@ -151,3 +151,29 @@ def test_run_lockstep_equals_threaded_run(p, c, variant):
         for name, v in ref.ledger.counters[prim].items():
             assert np.array_equal(got.ledger.counters[prim][name], v), (prim, name)
     assert got.ledger.pair_max_bytes == ref.ledger.pair_max_bytes
+
+
+def test_run_graph_multi_rank_equals_eager():
+    """Four ranks in one process: the captured lock-step epoch replays the
+    threaded runtime's results bit for bit, ledger included."""
+    from paper_2504_04673_b200 import graphgen
+    from paper_2504_04673_b200.gcn import GcnRun
+    a = P.gcn_normalize(graphgen.rmat(10, 8, 9))
+    a.values = a.values.astype(np.float32).astype(np.float64)
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((a.n_rows, 16)).astype(np.float32)
+    y = rng.integers(0, 4, a.n_rows)
+    cfg = P.TrainConfig(layers=3, hidden=16, lr=0.1, epochs=3, seed=4, variant="1d-sparse")
+    gr = GcnRun(a, x, y, np.ones(a.n_rows, bool), cfg, p=4)
+    ref = gr.result(gr.run())
+    for _ in range(2):
+        got = gr.result(gr.run_graph())
+        assert np.array_equal(got.losses, ref.losses)
+        for w1, w2 in zip(got.weights_per_rank, ref.weights_per_rank):
+            for a1, a2 in zip(w1, w2):
+                assert np.array_equal(a1, a2)
+        assert got.history == ref.history
+        for prim in ref.ledger.counters:
+            for name, v in ref.ledger.counters[prim].items():
+                assert np.array_equal(got.ledger.counters[prim][name], v), (prim, name)
+    gr.close()
