@@ -698,7 +698,8 @@ def run_ours(args, wl):
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
         "cuda_graph": bool(use_graph),
-        "host_driver": "lockstep" if lockstep else ("graph" if use_graph else "rank threads"),
+        "host_driver": ("graph" if use_graph else "") + ("+lockstep" if lockstep else "")
+                       if (use_graph or lockstep) else "rank threads",
         "epoch_breakdown_ms": breakdown,
         "extension_transform_first": None if tf_ms is None else {
             "epoch_ms": round(tf_ms, 3),
