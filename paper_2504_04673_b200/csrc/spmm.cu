@@ -461,9 +461,12 @@ LaunchFn pick_launch(int G, int CPL) {
   return nullptr;
 }
 
-// Tuning overrides for sweeps (scripts/spmm_sweep.py): DG_SPMM_MINB=3|4
-// raises the CTAs-per-SM target of the one-chunk-per-lane 256-bit fp64
-// kernels; DG_SPMM_FORCE="G,CPL" fixes the lane shape.  Read once.
+// Tuning overrides for sweeps (scripts/spmm_sweep.sh; unset in production,
+// read once): DG_SPMM_MINB=3|4 (CTAs/SM target of the one-chunk-per-lane
+// 256-bit kernels), DG_SPMM_E (entries per step), DG_SPMM_TWO / DG_SPMM_STG
+// (two-level fp32 sums / staged entries in the experiment grid),
+// DG_SPMM_FORCE_G + DG_SPMM_FORCE_CPL (lane shape), DG_SPMM_FORCE_V4
+// (128-bit lanes for wide rows).
 int env_int(const char* name, int dflt) {
   const char* e = std::getenv(name);
   return e ? std::atoi(e) : dflt;
