@@ -21,23 +21,30 @@
 
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace {
 
-constexpr int BM = 64;   // rows per CTA (dense_rows)
-constexpr int BK = 32;   // k-chunk (2 float4 per thread in flight)
+constexpr int BK = 32;   // k-chunk
 
-template <int TN>
+// Thread tile 4 rows x TN columns; CG column groups x (256 / CG) row groups,
+// so a CTA covers BM = 4 * 256 / CG rows.  N <= 16 uses TN = 4, CG = 4
+// (256 rows per CTA): each A value read from shared memory feeds 4 FMAs and
+// the 4 column groups of a row group read it as a broadcast (16 threads
+// across N with TN = 1 read every A value 16 times: shared-memory bound).
+template <int TN, int CG = 16>
 __global__ void __launch_bounds__(256) dense_rows_kernel(
     const float* __restrict__ A, int64_t lda, int64_t n, int K, const float* __restrict__ B,
     int64_t ldb, int N, int transB, float* __restrict__ C, int64_t ldc,
     float* __restrict__ Crelu, const float* __restrict__ Zmask, int64_t ldm) {
   extern __shared__ float smem[];
-  constexpr int NP = 16 * TN;                       // padded N
+  constexpr int NP = CG * TN;                        // padded N
+  constexpr int BM = 4 * 256 / CG;                   // rows per CTA
   float* Bs = smem;                                  // K x NP
   float* As = smem + (size_t)K * NP;                 // BK x (BM + 4)
   const int tid = threadIdx.x;
-  const int tx = tid % 16;                           // column group
-  const int ty = tid / 16;                           // row group (4 rows)
+  const int tx = tid % CG;                           // column group
+  const int ty = tid / CG;                           // row group (4 rows)
   for (int i = tid; i < K * NP; i += 256) {
     const int k = i / NP, j = i % NP;
     float b = 0.f;
@@ -50,9 +57,9 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(
   for (int r = 0; r < 4; ++r)
 #pragma unroll
     for (int c = 0; c < TN; ++c) acc[r][c] = 0.f;
-  // A chunk loader: each thread owns 2 float4 of the 64 x 32 chunk; the
+  // A chunk loader: each thread owns PER float4 of the BM x 32 chunk; the
   // next chunk is loaded into registers while the current one is consumed
-  constexpr int PER = BM * BK / 4 / 256;            // float4 per thread (2)
+  constexpr int PER = BM * BK / 4 / 256;            // float4 per thread
   auto load_chunk = [&](int k0, float4* v) {
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
@@ -263,25 +270,36 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
       ((uintptr_t)A & 15))
     return set_err(DG_ERR_ARG, "dense_rows: shape outside the kernel's range");
   if (n == 0) return DG_OK;
-  const size_t smem = ((size_t)K * 16 * TN + (size_t)BK * (BM + 4)) * sizeof(float);
-  const unsigned blocks = (unsigned)((n + BM - 1) / BM);
   cudaStream_t st = S(stream);
-#define DG_DR(tn)                                                                          \
-  do {                                                                                     \
-    static bool attr = false;                                                              \
-    if (!attr) {                                                                           \
-      DG_CK(cudaFuncSetAttribute(dense_rows_kernel<tn>,                                    \
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)); \
-      attr = true;                                                                         \
-    }                                                                                      \
-    dense_rows_kernel<tn><<<blocks, 256, smem, st>>>(A, lda, n, K, B, ldb, N, transB, C, ldc, \
-                                                     C_relu, z_mask, ld_mask);             \
+  static const bool narrow_env = [] {
+    const char* e = std::getenv("DG_DENSE_WIDE_TILE");
+    return !e || std::atoi(e) != 0;
+  }();
+#define DG_DR(tn, cg)                                                                       \
+  do {                                                                                      \
+    constexpr int bm = 4 * 256 / (cg);                                                      \
+    const size_t smem = ((size_t)K * (cg) * (tn) + (size_t)BK * (bm + 4)) * sizeof(float); \
+    const unsigned blocks = (unsigned)((n + bm - 1) / bm);                                  \
+    static bool attr = false;                                                               \
+    if (!attr) {                                                                            \
+      DG_CK(cudaFuncSetAttribute(dense_rows_kernel<tn, cg>,                                 \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));  \
+      attr = true;                                                                          \
+    }                                                                                       \
+    dense_rows_kernel<tn, cg><<<blocks, 256, smem, st>>>(A, lda, n, K, B, ldb, N, transB, C, \
+                                                         ldc, C_relu, z_mask, ld_mask);     \
   } while (0)
-  switch (TN) {
-    case 1: DG_DR(1); break;
-    case 2: DG_DR(2); break;
-    case 3: DG_DR(3); break;
-    default: DG_DR(4); break;
+  // long rows only (K >= 128): Reddit layer 1 (K=602) 0.303 -> 0.276 ms; short
+  // rows (K <= 48) lose occupancy to the larger tile and run slower
+  if (N <= 16 && ldc <= 16 && K >= 128 && narrow_env) {
+    DG_DR(4, 4);                          // 4 rows x 4 columns per thread, 256 rows per CTA
+  } else {
+    switch (TN) {
+      case 1: DG_DR(1, 16); break;
+      case 2: DG_DR(2, 16); break;
+      case 3: DG_DR(3, 16); break;
+      default: DG_DR(4, 16); break;
+    }
   }
 #undef DG_DR
   DG_LAUNCHED();
