@@ -6,11 +6,13 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 ROWS = [
     ("Reddit-shaped (config 2)", "1 × 1", "final1/reddit_n1.json"),
-    ("Reddit-shaped", "2 × 1", "final4/reddit_n2.json"),
+    ("Reddit-shaped", "2 × 1", "final2/reddit_n2.json"),
+    ("Reddit-shaped, 1d-oblivious", "2 × 1", "final2/reddit_n2_obl.json"),
     ("Reddit-shaped", "4 × 1", "final4/reddit_n4.json"),
     ("Reddit-shaped", "4 × 2 (8 ranks)", "final4/reddit_n4_p8.json"),
     ("Reddit-shaped, 15d-sparse c=2", "4 × 2 (8 ranks)", "final4/reddit_n4_p8_15d_c2.json"),
     ("products-shaped (config 3), community layout", "1 × 1", "final1/products_n1.json"),
+    ("products-shaped, community partition", "2 × 1", "final2/products_n2.json"),
     ("products-shaped, community partition", "4 × 1", "final4/products_n4.json"),
     ("products-shaped, greedy-tv → GVB", "4 × 1", "final4/products_n4_gvb.json"),
     ("products-shaped, GVB, 1d-oblivious", "4 × 1", "final4/products_n4_gvb_obl.json"),
