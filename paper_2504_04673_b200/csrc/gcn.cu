@@ -118,6 +118,12 @@ __device__ __forceinline__ double grp_sum(double v) {
   return v;
 }
 template <int G>
+__device__ __forceinline__ float grp_sumf(float v) {
+#pragma unroll
+  for (int o = G / 2; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+  return v;
+}
+template <int G>
 __device__ __forceinline__ int grp_min(int v) {
 #pragma unroll
   for (int o = G / 2; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o, G));
@@ -183,10 +189,10 @@ __global__ void __launch_bounds__(256, (K <= 2 ? 3 : 1)) xent_vec_kernel(
         for (int e = 0; e < 4; ++e) m = fmaxf(m, v[u][k][e]);
       m = grp_max<G>(m);
       const int64_t lbl = labels[row];
-      // per lane: an fp32 partial of its <= 4K exponentials (each in (0, 1]),
-      // then the lanes' partials summed in fp64
-      float sl = 0.f;
-      double xl = 0.0;
+      // the exponentials (each in (0, 1]) summed in fp32: a lane's <= 4K
+      // terms, then a fixed xor tree over the G lanes (<= (4K + log2 G) ulp);
+      // the label's logit comes from its owner lane with one shuffle
+      float sl = 0.f, xv = 0.f;
       int am = C;
 #pragma unroll
       for (int k = 0; k < K; ++k)
@@ -195,15 +201,18 @@ __global__ void __launch_bounds__(256, (K <= 2 ? 3 : 1)) xent_vec_kernel(
           const int j = 4 * (lig + k * G) + e;
           if (j < C) {
             if (v[u][k][e] == m && j < am) am = j;
-            if (j == lbl) xl = (double)v[u][k][e] - (double)m;
+            if (j == lbl) xv = v[u][k][e];
             v[u][k][e] = expf(v[u][k][e] - m);
             sl += v[u][k][e];
           } else {
             v[u][k][e] = 0.f;
           }
         }
-      const double s = grp_sum<G>((double)sl);
-      xl = grp_sum<G>(xl);
+      const double s = (double)grp_sumf<G>(sl);
+      const int owner = (int)((lbl >> 2) % G);
+      const double xl =
+          (double)__shfl_sync(0xffffffffu, xv, ((threadIdx.x & 31) & ~(G - 1)) + owner) -
+          (double)m;
       am = grp_min<G>(am);
       const bool on = valid[u] && mask[row] != 0;
       // (softmax - onehot) / denom with one division per row: p_j/denom =
