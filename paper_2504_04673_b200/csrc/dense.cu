@@ -265,11 +265,9 @@ extern "C" {
 int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float* B, int64_t ldb,
                   int32_t N, int32_t transB, float* C, int64_t ldc, float* C_relu,
                   const float* z_mask, int64_t ld_mask, void* stream) {
-  // N <= 64: TN = ceil(N / 16); wider outputs (papers-shaped C=172, padded
-  // to 192): TN = 8 or 12 (4 rows x TN columns per thread, 16 column groups)
-  const int TN = N <= 64 ? tn_of(N) : (N <= 128 ? 8 : 12);
-  if (n < 0 || K < 1 || N < 1 || N > 192 || (int64_t)K * 16 * TN > 16384 || (lda & 3) ||
-      ((uintptr_t)A & 15) || (N > 64 && ldc > 16 * TN))
+  const int TN = tn_of(N);
+  if (n < 0 || K < 1 || N < 1 || N > 64 || (int64_t)K * 16 * TN > 16384 || (lda & 3) ||
+      ((uintptr_t)A & 15))
     return set_err(DG_ERR_ARG, "dense_rows: shape outside the kernel's range");
   if (n == 0) return DG_OK;
   cudaStream_t st = S(stream);
@@ -300,9 +298,7 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
       case 1: DG_DR(1, 16); break;
       case 2: DG_DR(2, 16); break;
       case 3: DG_DR(3, 16); break;
-      case 4: DG_DR(4, 16); break;
-      case 8: DG_DR(8, 16); break;
-      default: DG_DR(12, 16); break;
+      default: DG_DR(4, 16); break;
     }
   }
 #undef DG_DR

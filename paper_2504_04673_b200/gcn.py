@@ -257,9 +257,7 @@ class _Dense:
 
     @staticmethod
     def _rows_ok(K, N):
-        """dg_dense_rows' range (N <= 192; B in shared memory)."""
-        tn = (N + 15) // 16 if N <= 64 else (8 if N <= 128 else 12)
-        return N <= 192 and K * 16 * tn <= 16384 and (N <= 64 or pad4(N) <= 16 * tn)
+        return N <= 64 and K * 16 * ((N + 15) // 16) <= 16384
 
     def fwd(self, t, w, f_in, f_out, relu, z=None):
         """z = t @ w (padded), h = relu(z) if requested (gcn.py:274-276);
