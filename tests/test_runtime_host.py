@@ -142,3 +142,15 @@ def test_runs_deterministic():
 
     a, b = P.run_program(4, 1, prog), P.run_program(4, 1, prog)
     assert a.results == b.results and a.ledger.to_dict() == b.ledger.to_dict()
+
+
+@pytest.mark.parametrize("kw", [dict(layers=1), dict(hidden=0), dict(lr=-0.1), dict(epochs=-1),
+                                dict(activation="tanh"), dict(order="sideways")])
+def test_train_config_validation(kw):
+    with pytest.raises(ValueError):
+        P.TrainConfig(**kw)
+
+
+def test_train_config_layer_dims():
+    cfg = P.TrainConfig(layers=4, hidden=16)
+    assert cfg.layer_dims(100, 47) == [100, 16, 16, 47]       # 3 weight matrices
