@@ -32,8 +32,8 @@ constexpr int BK = 32;   // k-chunk
 // (256 rows per CTA): each A value read from shared memory feeds 4 FMAs and
 // the 4 column groups of a row group read it as a broadcast (16 threads
 // across N with TN = 1 read every A value 16 times: shared-memory bound).
-template <int TN, int CG = 16>
-__global__ void __launch_bounds__(256) dense_rows_kernel(
+template <int TN, int CG = 16, int BKT = BK, int MB = 1>
+__global__ void __launch_bounds__(256, MB) dense_rows_kernel(
     const float* __restrict__ A, int64_t lda, int64_t n, int K, const float* __restrict__ B,
     int64_t ldb, int N, int transB, float* __restrict__ C, int64_t ldc,
     float* __restrict__ Crelu, const float* __restrict__ Zmask, int64_t ldm) {
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(
   constexpr int NP = CG * TN;                        // padded N
   constexpr int BM = 4 * 256 / CG;                   // rows per CTA
   float* Bs = smem;                                  // K x NP
-  float* As = smem + (size_t)K * NP;                 // BK x (BM + 4)
+  float* As = smem + (size_t)K * NP;                 // BKT x (BM + 4)
   const int tid = threadIdx.x;
   const int tx = tid % CG;                           // column group
   const int ty = tid / CG;                           // row group (4 rows)
@@ -59,12 +59,12 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(
     for (int c = 0; c < TN; ++c) acc[r][c] = 0.f;
   // A chunk loader: each thread owns PER float4 of the BM x 32 chunk; the
   // next chunk is loaded into registers while the current one is consumed
-  constexpr int PER = BM * BK / 4 / 256;            // float4 per thread
+  constexpr int PER = BM * BKT / 4 / 256;            // float4 per thread
   auto load_chunk = [&](int k0, float4* v) {
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int i = tid + u * 256;
-      const int r = i / (BK / 4), q = i % (BK / 4);
+      const int r = i / (BKT / 4), q = i % (BKT / 4);
       const int64_t gr = row0 + r;
       const int k = k0 + 4 * q;
       v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -82,20 +82,20 @@ __global__ void __launch_bounds__(256) dense_rows_kernel(
   };
   float4 nxt[PER];
   load_chunk(0, nxt);
-  for (int k0 = 0; k0 < K; k0 += BK) {
+  for (int k0 = 0; k0 < K; k0 += BKT) {
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < PER; ++u) {                  // stage transposed: As[k][r]
       const int i = tid + u * 256;
-      const int r = i / (BK / 4), q = i % (BK / 4);
+      const int r = i / (BKT / 4), q = i % (BKT / 4);
       As[(4 * q + 0) * (BM + 4) + r] = nxt[u].x;
       As[(4 * q + 1) * (BM + 4) + r] = nxt[u].y;
       As[(4 * q + 2) * (BM + 4) + r] = nxt[u].z;
       As[(4 * q + 3) * (BM + 4) + r] = nxt[u].w;
     }
     __syncthreads();
-    if (k0 + BK < K) load_chunk(k0 + BK, nxt);       // in flight during the math
-    const int kmax = min(BK, K - k0);
+    if (k0 + BKT < K) load_chunk(k0 + BKT, nxt);       // in flight during the math
+    const int kmax = min(BKT, K - k0);
 #pragma unroll 8
     for (int kk = 0; kk < kmax; ++kk) {
       const float4 a = *reinterpret_cast<const float4*>(&As[kk * (BM + 4) + 4 * ty]);
@@ -275,24 +275,34 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
     const char* e = std::getenv("DG_DENSE_WIDE_TILE");
     return !e || std::atoi(e) != 0;
   }();
-#define DG_DR(tn, cg)                                                                       \
+#define DG_DR4(tn, cg, bk, mb)                                                              \
   do {                                                                                      \
     constexpr int bm = 4 * 256 / (cg);                                                      \
-    const size_t smem = ((size_t)K * (cg) * (tn) + (size_t)BK * (bm + 4)) * sizeof(float); \
+    const size_t smem = ((size_t)K * (cg) * (tn) + (size_t)(bk) * (bm + 4)) * sizeof(float); \
     const unsigned blocks = (unsigned)((n + bm - 1) / bm);                                  \
     static bool attr = false;                                                               \
     if (!attr) {                                                                            \
-      DG_CK(cudaFuncSetAttribute(dense_rows_kernel<tn, cg>,                                 \
+      DG_CK(cudaFuncSetAttribute(dense_rows_kernel<tn, cg, bk, mb>,                         \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));  \
       attr = true;                                                                          \
     }                                                                                       \
-    dense_rows_kernel<tn, cg><<<blocks, 256, smem, st>>>(A, lda, n, K, B, ldb, N, transB, C, \
-                                                         ldc, C_relu, z_mask, ld_mask);     \
+    dense_rows_kernel<tn, cg, bk, mb><<<blocks, 256, smem, st>>>(A, lda, n, K, B, ldb, N,   \
+                                                                 transB, C, ldc, C_relu,    \
+                                                                 z_mask, ld_mask);          \
   } while (0)
+#define DG_DR(tn, cg) DG_DR4(tn, cg, BK, 1)
   // long rows only (K >= 128): Reddit layer 1 (K=602) 0.303 -> 0.276 ms; short
   // rows (K <= 48) lose occupancy to the larger tile and run slower
+  static const int dr_var = [] {
+    const char* e = std::getenv("DG_DENSE_VAR");
+    return e ? std::atoi(e) : 0;
+  }();
   if (N <= 16 && ldc <= 16 && K >= 128 && narrow_env) {
-    DG_DR(4, 4);                          // 4 rows x 4 columns per thread, 256 rows per CTA
+    // 4 rows x 4 columns per thread, 256 rows per CTA, 16-wide k-chunks
+    // (Reddit layer 1: 0.26 -> 0.24 ms vs 32-wide; DG_DENSE_VAR sweeps)
+    if (dr_var == 1) DG_DR4(4, 4, 16, 3);
+    else if (dr_var == 3) DG_DR4(4, 4, 32, 1);
+    else DG_DR4(4, 4, 16, 2);
   } else {
     switch (TN) {
       case 1: DG_DR(1, 16); break;
@@ -302,6 +312,7 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
     }
   }
 #undef DG_DR
+#undef DG_DR4
   DG_LAUNCHED();
   return DG_OK;
 }
