@@ -237,6 +237,109 @@ __global__ void __launch_bounds__(256) dense_tn_kernel(
   }
 }
 
+// N <= 16 (every hidden width): thread tile 4 k x 4 n; 64 k-groups x 4
+// n-groups cover a 256-wide K block.  Per row each thread reads one float4
+// of H and one of M (both broadcast within a warp) for 16 FMAs, instead of
+// 4 FMAs per two shared loads with 16 threads across N.
+constexpr int TN4_RC = 32;                  // rows per chunk
+
+__global__ void __launch_bounds__(256, 2) dense_tn4_kernel(
+    const float* __restrict__ H, int64_t ldh, int64_t n, int K, const float* __restrict__ M,
+    int64_t ldm, int N, int64_t rows_per, double* __restrict__ work) {
+  __shared__ __align__(16) float Hs[TN4_RC][256 + 4];
+  __shared__ __align__(16) float Ms[TN4_RC][16 + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid & 3;                            // columns 4 tx .. 4 tx + 3
+  const int ty = tid >> 2;                           // k = k0 + 4 ty .. + 3
+  const int k0 = blockIdx.y * 256;
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per;
+  const int64_t r_end = min(n, r_begin + rows_per);
+  float part[4][4];
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      part[i][c] = 0.f;
+      acc[i][c] = 0.0;
+    }
+  // chunk loaders: H 32 x 256 (8 float4 per thread), M 32 x 16 (half a float4)
+  auto load_chunk = [&](int64_t r0, float4* hv, float4& mv) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = tid + u * 256;
+      const int rr = i >> 6, q = i & 63;
+      const int64_t gr = r0 + rr;
+      const int k = k0 + 4 * q;
+      hv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (gr < r_end && k < K) {
+        const float* hp = H + gr * ldh + k;
+        if (k + 3 < K) {
+          hv[u] = __ldcs(reinterpret_cast<const float4*>(hp));
+        } else {
+          hv[u].x = hp[0];
+          if (k + 1 < K) hv[u].y = hp[1];
+          if (k + 2 < K) hv[u].z = hp[2];
+        }
+      }
+    }
+    mv = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid < TN4_RC * 4) {
+      const int rr = tid >> 2, q = tid & 3;
+      const int64_t gr = r0 + rr;
+      if (gr < r_end) {
+        const float* mp = M + gr * ldm + 4 * q;
+        float t[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) t[e] = (4 * q + e < N) ? mp[e] : 0.f;
+        mv = make_float4(t[0], t[1], t[2], t[3]);
+      }
+    }
+  };
+  float4 hv[8], mv;
+  if (r_begin < r_end) load_chunk(r_begin, hv, mv);
+  for (int64_t r0 = r_begin; r0 < r_end; r0 += TN4_RC) {
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = tid + u * 256;
+      *reinterpret_cast<float4*>(&Hs[i >> 6][4 * (i & 63)]) = hv[u];
+    }
+    if (tid < TN4_RC * 4) *reinterpret_cast<float4*>(&Ms[tid >> 2][4 * (tid & 3)]) = mv;
+    __syncthreads();
+    if (r0 + TN4_RC < r_end) load_chunk(r0 + TN4_RC, hv, mv);
+#pragma unroll 4
+    for (int rr = 0; rr < TN4_RC; ++rr) {
+      const float4 h = *reinterpret_cast<const float4*>(&Hs[rr][4 * ty]);
+      const float4 m = *reinterpret_cast<const float4*>(&Ms[rr][4 * tx]);
+      const float hh[4] = {h.x, h.y, h.z, h.w};
+      const float mm[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) part[i][c] = fmaf(hh[i], mm[c], part[i][c]);
+    }
+    if (((r0 - r_begin) / TN4_RC) % 2 == 1 || r0 + TN4_RC >= r_end) {   // 64-row windows
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[i][c] += (double)part[i][c];
+          part[i][c] = 0.f;
+        }
+    }
+  }
+  // work layout: [slice][K][16]
+  double* wp = work + (int64_t)blockIdx.x * K * 16;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = k0 + 4 * ty + i;
+    if (k >= K) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) wp[(int64_t)k * 16 + 4 * tx + c] = acc[i][c];
+  }
+}
+
 // One warp per output element: lane l sums slices l, l+32, ... in order,
 // then a fixed xor tree -- deterministic, and the slices' partials are read
 // 32 at a time instead of one dependent load per slice.
@@ -317,11 +420,24 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
   return DG_OK;
 }
 
-int64_t dg_dense_tn_work(int64_t n, int32_t K, int32_t N) {
-  const int kb = (K + 63) / 64;
+// the 256-wide K blocks pay only when they are mostly full: Reddit layer 1
+// (K=608) 0.29 -> 0.24 ms; K <= 100 ran up to 2.4x slower (idle k-groups)
+static bool tn4_ok(int32_t N, int32_t K) {
+  static const bool env = [] {
+    const char* e = std::getenv("DG_DENSE_TN4");
+    return !e || std::atoi(e) != 0;
+  }();
+  return N <= 16 && K >= 256 && env;
+}
+
+static int64_t tn_slices(int64_t n, int32_t K, int32_t N) {
+  const int kb = tn4_ok(N, K) ? (K + 255) / 256 : (K + 63) / 64;
   int64_t slices = std::max<int64_t>(1, (4 * 148) / kb);
-  slices = std::min<int64_t>(slices, std::max<int64_t>(1, (n + 255) / 256));
-  return slices * (int64_t)K * 16 * tn_of(N) * nblk_of(N);
+  return std::min<int64_t>(slices, std::max<int64_t>(1, (n + 255) / 256));
+}
+
+int64_t dg_dense_tn_work(int64_t n, int32_t K, int32_t N) {
+  return tn_slices(n, K, N) * (int64_t)K * 16 * tn_of(N) * nblk_of(N);
 }
 
 int dg_dense_tn(const float* H, int64_t ldh, int64_t n, int32_t K, const float* M, int64_t ldm,
@@ -333,15 +449,17 @@ int dg_dense_tn(const float* H, int64_t ldh, int64_t n, int32_t K, const float* 
   if (n < 0 || K < 1 || N < 1 || N > 256 || (ldh & 3) || ((uintptr_t)H & 15) || ldy > NPT ||
       ldy < N)
     return set_err(DG_ERR_ARG, "dense_tn: shape outside the kernel's range");
-  const int kb = (K + 63) / 64;
-  int64_t slices = std::max<int64_t>(1, (4 * 148) / kb);
-  slices = std::min<int64_t>(slices, std::max<int64_t>(1, (n + 255) / 256));
+  const bool t4 = tn4_ok(N, K);
+  const int kb = t4 ? (K + 255) / 256 : (K + 63) / 64;
+  const int64_t slices = tn_slices(n, K, N);
   if (work_len < slices * (int64_t)K * NPT)
     return set_err(DG_ERR_ARG, "dense_tn: work buffer too small");
   const int64_t rows_per = std::max<int64_t>(1, (n + slices - 1) / slices);
   const dim3 grid((unsigned)slices, (unsigned)kb, (unsigned)NB);
   cudaStream_t st = S(stream);
-  switch (TN) {
+  if (t4) {
+    dense_tn4_kernel<<<grid, 256, 0, st>>>(H, ldh, n, K, M, ldm, N, rows_per, work);
+  } else switch (TN) {
     case 1: dense_tn_kernel<1><<<grid, 256, 0, st>>>(H, ldh, n, K, M, ldm, N, rows_per, work); break;
     case 2: dense_tn_kernel<2><<<grid, 256, 0, st>>>(H, ldh, n, K, M, ldm, N, rows_per, work); break;
     case 3: dense_tn_kernel<3><<<grid, 256, 0, st>>>(H, ldh, n, K, M, ldm, N, rows_per, work); break;
