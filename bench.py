@@ -626,12 +626,14 @@ def run_ours(args, wl):
     # epoch k computes (double-buffered input pipeline); step 0's upload is
     # exposed.  All copies are inside the timed region.
     rows = [gr.dm.boundaries[grid.coords(r)[0]] for r in dp.local]
-    # the step's inputs cross PCIe unpadded (n x f_in fp32); the device
-    # scatters them into the padded row pitch
-    f_in = dims[0]
+    # when the row pitch pads the features noticeably (products: 100 -> 128),
+    # the step's inputs cross PCIe unpadded and the device scatters them into
+    # the padded pitch; otherwise (Reddit: 602 -> 608) they are uploaded as is
+    f_in = dims[0] if gr.x.shape[1] > 1.05 * dims[0] else gr.x.shape[1]
     xh = {r: gr.x[r0:r1, :f_in].contiguous().cpu().pin_memory()
           for r, (r0, r1) in zip(dp.local, rows)}
-    stage = {r: torch.empty_like(xh[r], device=gr.x.device) for r in dp.local}
+    stage = ({r: torch.empty_like(xh[r], device=gr.x.device) for r in dp.local}
+             if f_in < gr.x.shape[1] else None)
     xbuf = [gr.x, torch.zeros_like(gr.x)]
     copy_stream = torch.cuda.Stream()
     e2e_steps = max(2, args.steps)               # the same K as the device-timed region
@@ -641,8 +643,11 @@ def run_ours(args, wl):
     def upload(buf, stream):
         with torch.cuda.stream(stream):
             for r, (r0, r1) in zip(dp.local, rows):
-                stage[r].copy_(xh[r], non_blocking=True)
-                buf[r0:r1, :f_in].copy_(stage[r])
+                if stage is None:
+                    buf[r0:r1].copy_(xh[r], non_blocking=True)
+                else:
+                    stage[r].copy_(xh[r], non_blocking=True)
+                    buf[r0:r1, :f_in].copy_(stage[r])
         ev = torch.cuda.Event()
         ev.record(stream)
         return ev
