@@ -248,35 +248,203 @@ def host_info():
     return info
 
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+# scaled-down samples for the reference arm (same average degree
+# and widths as the full graph, nnz small enough that one epoch of the
+# unchanged reference takes a few seconds on the box's cores)
+REF_SAMPLES = {
+    "reddit": dict(n_full=232_965, nnz_full=114_848_856, alpha=0.6, cap=21_657, n=4096),
+    "products": dict(n_full=2_449_029, nnz_full=123_718_280, alpha=0.55, cap=17_481,
+                     n=65_536),
+    "papers": dict(n_full=111_059_956, nnz_full=3_230_000_000, alpha=0.7, cap=30_000,
+                   n=131_072),
+}
+
+
+def import_reference():
+    """The unmodified reference package installed in baseline/_ref
+    (`pip install --no-deps --target baseline/_ref <copy of /root/reference/pkg>`),
+    or None when it is absent."""
+    if not os.path.isdir(os.path.join(REF_DIR, "distgcn")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    import distgcn
+    if not os.path.abspath(distgcn.__file__).startswith(os.path.abspath(REF_DIR)):
+        raise SystemExit(f"distgcn imported from {distgcn.__file__}, not baseline/_ref")
+    return distgcn
+
+
+def ref_epoch_times(D, a_hat, x, y, cfg_kw, p, epochs):
+    """Wall time of each epoch of the unchanged reference `distgcn.train`
+    (gcn.py:230-302) at p simulated ranks.  Observation only: the per-epoch
+    `Comm.ledger_mark` collective (gcn.py:285) is wrapped to timestamp its
+    completion on rank 0 -- the moment every rank has finished the epoch.
+    Returns (per-epoch seconds, TrainResult)."""
+    stamps = []
+    orig = D.runtime.Comm.ledger_mark
+
+    def timed_mark(self, label):
+        orig(self, label)
+        if self.rank == 0:
+            stamps.append(time.perf_counter())
+
+    cfg = D.TrainConfig(epochs=epochs, **cfg_kw)
+    D.runtime.Comm.ledger_mark = timed_mark
+    try:
+        t0 = time.perf_counter()
+        res = D.train(a_hat, x, y, np.ones(a_hat.n_rows, bool), cfg, p=p)
+    finally:
+        D.runtime.Comm.ledger_mark = orig
+    ts = [t0] + stamps
+    return [b - a for a, b in zip(ts[:-1], ts[1:])], res
+
+
+def reference_measure(args, wl, warmup, steps):
+    """Time the unchanged reference (see run_reference).  Returns a dict:
+    value (full-workload ms per epoch), ms (measured per-step ms), kind,
+    sample, cores, timed (per-epoch seconds), extra."""
+    D = import_reference()
+    if D is None:
+        return None
+    from paper_2504_04673_b200 import graphgen
+    cores = os.cpu_count() or 1
+    cfg_kw = dict(layers=wl["layers"], hidden=wl["hidden"], lr=0.01, seed=1,
+                  variant=args.variant)
+    if args.workload == "rmat14":
+        p = args.gpus * args.ranks_per_gpu
+        n, u, v = graphgen.rmat_edges(14, 16, 0)
+        a = D.gcn_normalize(_ref_csr(D, graphgen.symmetric_unit(n, u, v)))
+        x, y, _ = make_inputs(wl, n)
+        ep, res = ref_epoch_times(D, a, x, y, cfg_kw, p, warmup + steps)
+        timed = ep[warmup:]
+        ms = statistics.median(timed) * 1e3
+        return dict(value=ms, ms=ms, kind="measured (full workload)", cores=p, timed=timed,
+                    sample=(f"full config 1: unchanged distgcn.train (baseline/_ref), "
+                            f"R-MAT-14, {a.nnz:,} nnz, p={p} simulated ranks (threads), "
+                            f"{args.variant}"),
+                    extra={"ref_p": p, "nnz": int(a.nnz),
+                           "loss_first_last": [res.losses[0], res.losses[-1]]})
+    sp = REF_SAMPLES[args.workload]
+    p = min(cores, 16)
+    deg = sp["nnz_full"] / sp["n_full"]
+
+    def sample_graph(ns):
+        g = graphgen.chung_lu_host(ns, int(ns * deg / 2), alpha=sp["alpha"],
+                                   max_weight=sp["cap"] * ns / sp["n_full"], seed=0)
+        return D.gcn_normalize(_ref_csr(D, g))
+
+    a = sample_graph(sp["n"])
+    x, y, _ = make_inputs(wl, a.n_rows)
+    log(f"[bench] reference sample: n={a.n_rows} nnz={a.nnz:,}, p={p} threads")
+    ep, _ = ref_epoch_times(D, a, x, y, cfg_kw, p, warmup + steps)
+    timed = ep[warmup:]
+    sample_ms = statistics.median(timed) * 1e3
+    full_nnz = sp["nnz_full"] + sp["n_full"]          # + self-loops (gcn_normalize)
+    scale = full_nnz / a.nnz
+    # linearity check: a half-size sample, 3 epochs (first discarded)
+    a2 = sample_graph(sp["n"] // 2)
+    x2, y2, _ = make_inputs(wl, a2.n_rows)
+    ep2, _ = ref_epoch_times(D, a2, x2, y2, cfg_kw, p, 3)
+    half_ms = statistics.median(ep2[1:]) * 1e3
+    return dict(
+        value=sample_ms * scale, ms=sample_ms, cores=p, timed=timed,
+        kind="estimate (measured sample epoch x full nnz / sample nnz)",
+        sample=(f"unchanged distgcn.train (baseline/_ref) on a scaled-down "
+                f"{args.workload}-shaped Chung-Lu graph: n={a.n_rows:,}, nnz={a.nnz:,} "
+                f"(avg degree {a.nnz / a.n_rows:.0f}, same widths {wl['f_in']}/"
+                f"{wl['hidden']}/{wl['classes']}), p={p} simulated ranks = {p} threads, "
+                f"{args.variant}; value = median sample epoch x {scale:,.1f} "
+                f"(full nnz {full_nnz:,} / sample nnz)"),
+        extra={"ref_p": p, "sample_nnz": int(a.nnz), "sample_epoch_ms": round(sample_ms, 1),
+               "scale_to_full": round(scale, 3),
+               "linearity": {"half_sample_nnz": int(a2.nnz),
+                             "half_sample_epoch_ms": round(half_ms, 1),
+                             "ms_per_mnnz_sample": round(sample_ms / a.nnz * 1e6, 2),
+                             "ms_per_mnnz_half_sample": round(half_ms / a2.nnz * 1e6, 2)}})
+
+
+def cpu_baseline_entry(args, wl, a_hat=None, nnz_total=None):
+    """`cpu_baseline` of our arm: the unchanged reference (baseline/_ref) on
+    a bounded sample (1 warm-up + 3 timed epochs), else the oracle port's
+    np.add.at rate (kind "port")."""
+    m = reference_measure(args, wl, 1, 3)
+    if m is not None:
+        return {"value": round(m["value"], 1), "unit": "ms", "cores": m["cores"],
+                "kind": "reference", "value_kind": m["kind"], "sample": m["sample"],
+                "host": host_info(), **m["extra"]}
+    if a_hat is None:
+        return None
+    cms, rates, sample = cpu_reference_epoch_ms(a_hat, wl, budget_s=args.ref_budget,
+                                                nnz_total=nnz_total)
+    return {"value": round(cms, 1), "unit": "ms", "cores": 1, "kind": "port",
+            "sample": sample, "host": host_info()}
+
+
 def run_reference(args, wl):
+    """--impl reference: the reference's own CPU implementation, unchanged,
+    from baseline/_ref, on the box's host cores.  Rank 0 only.
+
+    * rmat14 (config 1): the full workload -- `distgcn.train` at the
+      config's p=4 ranks -- timed directly; `value` is measured.
+    * reddit / products / papers (configs 2, 3, 5): the reference cannot run
+      them at full size (np.add.at temporaries of nnz*f*8 bytes: ~554 GB for
+      Reddit) nor within minutes, so every step is one epoch of the unchanged
+      `train` on a scaled-down graph of the same shape (same generator law,
+      average degree and layer widths), with p = the host's core count so
+      every core is busy (the reference's ranks are threads; np.add.at
+      releases the GIL).  `ms_per_step` is that measured sample epoch;
+      `value` scales it to the full graph by nnz (the epoch is np.add.at
+      work, linear in nnz*f at fixed widths; a second, half-size sample is
+      timed to show the linearity) and is labelled an estimate."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    a_hat = make_graph(args.workload)
-    t0 = time.time()
-    vals = []
-    per_step = max(2.0, 4 * args.ref_budget / (args.warmup + args.steps))
-    for _ in range(args.warmup + args.steps):
-        ms, rates, sample = cpu_reference_epoch_ms(a_hat, wl, budget_s=per_step)
-        vals.append(ms)
-    ms = statistics.median(vals[args.warmup:])
+    t_all = time.time()
+    clk = ClockSampler(0) if _has_nvidia_smi() else None
+    m = reference_measure(args, wl, args.warmup, args.steps)
+    clocks = clk.stop() if clk is not None else None
+    if m is None:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "baseline/_ref (the reference package) is not installed"}))
+        return 0
     line = {
-        "metric": "gcn_epoch_ms", "value": round(ms, 3), "unit": "ms", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(ms, 3),
+        "metric": "gcn_epoch_ms", "value": round(m["value"], 3), "unit": "ms",
+        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(m["ms"], 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": wl["desc"], "variant": args.variant,
-                   "p": args.gpus * args.ranks_per_gpu, "c": args.c},
-        "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": 1, "kind": "port",
-                         "sample": sample, "host": host_info(),
-                         "rates_nnz_f_per_s": {str(k): round(v) for k, v in rates.items()}},
-        "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0,
+        "config": bench_config(args, wl),
+        "value_kind": m["kind"],
+        "cpu_baseline": {"value": round(m["value"], 3), "unit": "ms", "cores": m["cores"],
+                         "kind": "reference", "sample": m["sample"], "host": host_info(),
+                         **m["extra"]},
+        "e2e": {"value": round(m["value"], 3), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "wall_s": round(time.time() - t0, 1),
+        "epoch_s_each": [round(t, 3) for t in m["timed"]],
+        "clocks": clocks,
+        "wall_s": round(time.time() - t_all, 1),
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _has_nvidia_smi():
+    import shutil
+    return shutil.which("nvidia-smi") is not None
+
+
+def _ref_csr(D, a):
+    """Our CsrMatrix -> the reference's CsrMatrix (same arrays)."""
+    return D.CsrMatrix(a.n_rows, a.n_cols, np.asarray(a.row_ptr, np.int64),
+                       np.asarray(a.col_idx, np.int64), np.asarray(a.values, np.float64))
+
+
+def bench_config(args, wl):
+    """The `config` dict, identical in both arms (run details go elsewhere)."""
+    p = args.gpus * args.ranks_per_gpu
+    return {"workload": wl["desc"], "variant": args.variant, "p": p, "c": args.c}
 
 
 # ---------------------------------------------------------------------------
@@ -436,12 +604,7 @@ def run_papers(args, wl):
                 "busiest_rank_bytes": int(inter), "f": f0}
     cpu = None
     if lead and not args.no_cpu_baseline:
-        cms, rates, smp = cpu_reference_epoch_ms(sample, wl, budget_s=args.ref_budget,
-                                                 nnz_total=g.nnz_total)
-        cpu = {"value": round(cms, 1), "unit": "ms", "cores": 1, "kind": "port",
-               "sample": smp.replace("leading-row samples",
-                                     f"a {sample.nnz:,}-nnz leading-row sample of block 0 "
-                                     "(columns compacted)") + " -- full-graph estimate"}
+        cpu = cpu_baseline_entry(args, wl, sample, nnz_total=g.nnz_total)
     if not lead:
         return 0
     line = {
@@ -449,12 +612,12 @@ def run_papers(args, wl):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_epoch, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wl["desc"], "variant": args.variant, "p": p, "c": 1,
-                   "partition": "block (partition.py:154-161)",
-                   "l2": "inputs larger than L2 (H0 = %d MB per GPU)"
-                         % (sum(t.numel() for t in gr.x.values()) * 4 // 2**20),
-                   "ranks_per_gpu": args.ranks_per_gpu,
-                   "halo": "single-buffered (one extra device barrier per phase)"},
+        "config": bench_config(args, wl),
+        "run_config": {"partition": "block (partition.py:154-161)",
+                       "l2": "inputs larger than L2 (H0 = %d MB per GPU)"
+                             % (sum(t.numel() for t in gr.x.values()) * 4 // 2**20),
+                       "ranks_per_gpu": args.ranks_per_gpu,
+                       "halo": "single-buffered (one extra device barrier per phase)"},
         "spmm_hbm_gbs": round(spmm_bytes_epoch / (ms_epoch / 1e3) / 1e9, 1),
         "comm_elements_per_epoch": {"aware": int(aware), "oblivious": int(obl),
                                     "ratio": round(aware / obl, 4) if obl else None},
@@ -676,9 +839,7 @@ def run_ours(args, wl):
     # ---- CPU baseline (rank 0, N=1 only) --------------------------------
     cpu = None
     if lead and args.gpus == 1 and not args.no_cpu_baseline:
-        cms, rates, sample = cpu_reference_epoch_ms(a_hat, wl, budget_s=args.ref_budget)
-        cpu = {"value": round(cms, 1), "unit": "ms", "cores": 1, "kind": "port",
-               "sample": sample, "host": host_info()}
+        cpu = cpu_baseline_entry(args, wl, a_hat)
     if not lead:
         return 0
     line = {
@@ -686,11 +847,11 @@ def run_ours(args, wl):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_epoch, 3), "higher_is_better": False, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wl["desc"], "variant": args.variant, "p": p, "c": c,
-                   "reduce_after_transform": bool(args.reduce_after_transform),
-                   "partition": part_name,
-                   "l2": "inputs larger than L2 (H0 = %d MB)" % (gr.x.numel() * 4 // 2**20),
-                   "ranks_per_gpu": args.ranks_per_gpu},
+        "config": bench_config(args, wl),
+        "run_config": {"reduce_after_transform": bool(args.reduce_after_transform),
+                       "partition": part_name,
+                       "l2": "inputs larger than L2 (H0 = %d MB)" % (gr.x.numel() * 4 // 2**20),
+                       "ranks_per_gpu": args.ranks_per_gpu},
         "spmm_hbm_gbs": round(spmm_bytes_epoch / (ms_epoch / 1e3) / 1e9, 1),
         "comm_elements_per_epoch": {"aware": int(aware), "oblivious": int(obl),
                                     "ratio": round(aware / obl, 4) if obl else None},
@@ -735,7 +896,9 @@ def main():
     ap.add_argument("--variant", default="1d-sparse")
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ranks-per-gpu", type=int, default=1)
+    ap.add_argument("--ranks-per-gpu", type=int, default=None,
+                    help="virtual ranks per GPU (default 1; rmat14: p=4 ranks in total, "
+                         "config 1)")
     ap.add_argument("--c", type=int, default=1, help="1.5D replication factor")
     ap.add_argument("--no-transform-first", action="store_true")
     ap.add_argument("--reduce-after-transform", action="store_true",
@@ -747,6 +910,8 @@ def main():
                          "gvb: the reference's greedy-tv -> GVB")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
+    if args.ranks_per_gpu is None:
+        args.ranks_per_gpu = max(1, 4 // args.gpus) if args.workload == "rmat14" else 1
     if args.impl == "reference":
         return run_reference(args, wl)
     return run_ours(args, wl)

@@ -260,8 +260,13 @@ __global__ void barrier_kernel(const __grid_constant__ BArgs a) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
       if (v >= a.epoch) break;
       if (gtimer() - t0 > (uint64_t)a.timeout_ns) {
+        // Fail closed: a stalled peer means the halos / partial slots the
+        // following kernels read are stale.  Record the cause, then trap so
+        // the context faults and every later launch (and the host's next
+        // sync) reports the error instead of computing on stale data.
         atomicExch(a.err, 1);
-        break;
+        __threadfence_system();
+        __trap();
       }
     }
   }

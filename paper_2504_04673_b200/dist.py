@@ -13,6 +13,16 @@ every process maps every peer's buffers.  A pack kernel then stores rows
 straight into the peer's halo over NVLink; `barrier()` is a device kernel
 over IPC-mapped flag words (bounded spin, no host round trip).  The host
 side only exchanges the 64-byte IPC handles (gloo) once per buffer.
+
+Co-located processes (more processes than GPUs, e.g. the driver's 1-GPU
+test box running 2 or 4 processes on cuda:0) never run the device barrier:
+two kernels that spin on each other's flags from different contexts on one
+GPU have no co-scheduling guarantee (time-sliced contexts; on B200 such
+pairs raised Xid 109).  There `barrier()` is host-side instead -- finish
+this process's work on the current stream, then a gloo barrier -- and every
+other piece of the multi-process data path (IPC-mapped halos, peer stores,
+parity double-buffering, split own/halo SpMM, the cross-process reducers)
+runs unchanged.  `DG_BARRIER=device|host` overrides the choice.
 """
 
 from __future__ import annotations
@@ -41,6 +51,7 @@ class World:
         self._epoch = 0
         self._err = None
         self.device = None
+        self.barrier_mode = "device"
 
     @property
     def multi(self) -> bool:
@@ -70,6 +81,15 @@ class World:
                     pass
         self._flags = SymBuffer(self, 8 * self.size)
         self._err = torch.zeros(1, dtype=torch.int32, device=self.device)
+        uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+        colocated = len(set(self.all_gather_object(uuid))) < self.size
+        mode = os.environ.get("DG_BARRIER", "host" if colocated else "device")
+        if mode not in ("device", "host"):
+            raise ValueError(f"DG_BARRIER must be 'device' or 'host', got {mode!r}")
+        if mode == "device" and colocated:
+            raise ValueError("DG_BARRIER=device with several processes on one GPU: spinning "
+                             "kernels in different contexts are not co-scheduled")
+        self.barrier_mode = mode
         return self
 
     def all_gather_object(self, obj):
@@ -86,8 +106,14 @@ class World:
             dist.barrier(group=self._pg)
 
     def barrier(self):
-        """Device-side barrier of all processes, on the current stream."""
+        """Barrier of all processes, ordered on the current stream: a device
+        kernel over the IPC flag words, or (co-located processes) a stream
+        synchronize followed by a host barrier."""
         if not self.multi:
+            return
+        if self.barrier_mode == "host":
+            torch.cuda.current_stream().synchronize()
+            self.host_barrier()
             return
         self._epoch += 1
         ptrs = (C.c_void_p * self.size)(*self._flags.ptrs)

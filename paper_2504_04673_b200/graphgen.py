@@ -17,7 +17,7 @@ import numpy as np
 from .sparse import CsrMatrix
 
 __all__ = ["rmat_edges", "rmat", "reddit_shaped", "products_shaped", "symmetric_unit",
-           "gaussian_features", "clique_blocks", "sbm", "planted_partition"]
+           "gaussian_features", "clique_blocks", "sbm", "planted_partition", "chung_lu_host"]
 
 GRAPH500 = (0.57, 0.19, 0.19)
 
@@ -244,6 +244,35 @@ def chung_lu_device(n, pairs, alpha=0.6, max_weight=None, seed=0, communities=0,
     del keys, rows, cols, key2, rp
     torch.cuda.empty_cache()
     return (out, comm_host) if return_communities else out
+
+
+def chung_lu_host(n, pairs, alpha=0.6, max_weight=None, seed=0) -> CsrMatrix:
+    """Host (NumPy) Chung-Lu graph with exactly `pairs` undirected edges and
+    the same degree law as `chung_lu_device` (rank-k weight ~ (k+1)^-alpha,
+    capped, randomly relabelled).  Used for the CPU reference arm's
+    scaled-down samples of configs 2, 3 and 5 (same average degree), where
+    no device may be involved."""
+    rng = np.random.default_rng(seed)
+    w = (np.arange(n, dtype=np.float64) + 1.0) ** (-alpha)
+    w = w / w.sum() * (2.0 * pairs)
+    if max_weight is not None:
+        for _ in range(8):
+            w = np.minimum(w, float(max_weight))
+            w = w / w.sum() * (2.0 * pairs)
+    w = w[rng.permutation(n)]
+    cdf = np.cumsum(w)
+    cdf /= cdf[-1]
+    keys = np.zeros(0, dtype=np.int64)
+    while keys.size < pairs:
+        m = int((pairs - keys.size) * 1.3) + 4096
+        u = np.minimum(np.searchsorted(cdf, rng.random(m)), n - 1)
+        v = np.minimum(np.searchsorted(cdf, rng.random(m)), n - 1)
+        ok = u != v
+        u, v = u[ok], v[ok]
+        keys = np.unique(np.concatenate([keys, np.minimum(u, v) * n + np.maximum(u, v)]))
+    if keys.size > pairs:
+        keys = np.sort(rng.choice(keys, size=pairs, replace=False))
+    return symmetric_unit(n, keys // n, keys % n)
 
 
 def reddit_shaped_device(seed=0, n=232_965, nnz=114_848_856):

@@ -7,9 +7,13 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+@pytest.mark.skipif(not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "distgcn")),
+                    reason="baseline/_ref (the reference install) is absent")
 def test_reference_arm_line_rmat14():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
                         "--workload", "rmat14", "--steps", "1", "--warmup", "1",
@@ -21,7 +25,9 @@ def test_reference_arm_line_rmat14():
     assert line["higher_is_better"] is False
     assert line["value"] > 0 and line["ms_per_step"] == line["value"]
     cb = line["cpu_baseline"]
-    assert cb["kind"] == "port" and cb["cores"] == 1 and cb["value"] == line["value"]
+    # the unchanged reference (baseline/_ref) at config 1's p=4 ranks, timed in full
+    assert cb["kind"] == "reference" and cb["cores"] == 4 and cb["value"] == line["value"]
+    assert line["value_kind"].startswith("measured")
     assert line["e2e"] == {"value": line["value"], "unit": "ms", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     assert "R-MAT" in line["config"]["workload"]

@@ -1,5 +1,14 @@
 """Multi-process (torchrun, one process per GPU) parity: runs
-tests/mp_gpu_worker.py on 2 GPUs when the box has them."""
+tests/mp_gpu_worker.py with 2 and 4 processes against the reference's golden
+vectors.
+
+On a box with fewer GPUs than processes, World.init maps LOCAL_RANK onto
+LOCAL_RANK % device_count, so several processes share one device.  CUDA IPC
+works between processes on the same device, so the multi-process data path
+(IPC-mapped halos and parity double-buffering, the device barrier across the
+side and main streams, the split own-block / halo SpMM with beta=1, the
+cross-process GroupReducer / RowGroupReducer, the sharded builder) runs
+unchanged on a 1-GPU box -- only the transport is HBM instead of NVLink."""
 
 import os
 import subprocess
@@ -11,17 +20,17 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _ngpu():
+@pytest.mark.parametrize("nproc", [2, 4])
+def test_multiprocess_matches_reference(nproc):
     import torch
-    return torch.cuda.device_count()
-
-
-@pytest.mark.skipif(_ngpu() < 2 if __import__("torch").cuda.is_available() else True,
-                    reason="needs >= 2 GPUs")
-def test_two_gpu_processes_match_reference():
-    n = min(_ngpu(), 4)
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29617",
+    ngpu = torch.cuda.device_count()
+    env = dict(os.environ, OMP_NUM_THREADS="2")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1",
+           "--master-port", str(29617 + nproc),
            os.path.join(ROOT, "tests", "mp_gpu_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-4000:]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, env=env)
+    out = r.stdout[-6000:] + r.stderr[-6000:]
+    print(f"[{nproc} processes on {min(ngpu, nproc)} GPU(s)]\n" + r.stdout[-3000:])
+    assert r.returncode == 0, out
+    assert out.count("0 failures") == nproc, out
