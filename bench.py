@@ -402,9 +402,10 @@ def run_reference(args, wl):
     if rank != 0:
         return 0
     t_all = time.time()
-    clk = ClockSampler(0) if _has_nvidia_smi() else None
     m = reference_measure(args, wl, args.warmup, args.steps)
-    clocks = clk.stop() if clk is not None else None
+    # a CPU-only arm: the GPU idles, so its SM clocks say nothing about this run
+    clocks = {"note": "CPU-only arm (the reference is NumPy on the host cores); GPU clocks "
+                      "not applicable", "host": host_info()}
     if m is None:
         print(json.dumps({"impl": "reference", "unavailable":
                           "baseline/_ref (the reference package) is not installed"}))
@@ -638,7 +639,7 @@ def run_papers(args, wl):
         "peak_mem_gib": round(peak_mem / 2**30, 1),
         "setup_s": round(t_setup, 1),
         "clocks": clocks,
-        "loss": [round(v, 6) for v in res.losses.tolist()],
+        "loss": [float(v) for v in res.losses.tolist()],
         "nnz": int(g.nnz_total),
     }
     print(json.dumps(line), flush=True)
@@ -879,7 +880,7 @@ def run_ours(args, wl):
                     "same function, forward exchange at the narrow width (volume below the "
                     "reference's aware count); not the reference's order, not the headline"},
         "clocks": clocks,
-        "loss": [round(v, 6) for v in res.losses.tolist()],
+        "loss": [float(v) for v in res.losses.tolist()],
         "nnz": int(a_hat.nnz),
     }
     print(json.dumps(line), flush=True)
