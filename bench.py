@@ -112,7 +112,6 @@ def peaks():
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
 
 
-_COMM = {}
 
 
 def make_graph(name, seed=0):
@@ -122,7 +121,7 @@ def make_graph(name, seed=0):
     if name == "reddit":
         a = graphgen.reddit_shaped_device(seed=seed)
     elif name == "products":
-        a, _COMM["products"] = graphgen.products_shaped_device(seed=seed)
+        a, _ = graphgen.products_shaped_device(seed=seed)   # planted labels unused
     else:
         a = graphgen.rmat(14, 16, seed)
     log(f"[bench] graph {name}: n={a.n_rows} nnz={a.nnz} ({time.time() - t:.1f}s)")
@@ -679,12 +678,21 @@ def run_ours(args, wl):
         t_p = time.time()
         part = P.volume_balanced_refine(a_hat, P.greedy_tv_partition(a_hat, k))
         part_name = f"greedy-tv -> GVB (native, {time.time() - t_p:.0f}s host)"
-    elif args.workload in _COMM:
-        # community-ordered layout (also for a single part: locality)
-        from paper_2504_04673_b200.graphgen import community_partition
-        part = community_partition(_COMM[args.workload], k)
-        part_name = "planted-community, community-ordered (stand-in for METIS)"
-    gr = GcnRun(a_hat, x, y, mask, cfg, p=p, c=c, partition=part)
+    elif args.partition == "lpa" or (args.partition == "auto" and args.workload == "products"):
+        # graph-derived communities (label propagation on the GPU) packed onto
+        # k parts, every part community-ordered (also for k=1: locality)
+        from paper_2504_04673_b200.locality import lpa_partition
+        t_p = time.time()
+        part = lpa_partition(a_hat, k)
+        part_name = (f"label-propagation communities -> {k} parts, community-ordered "
+                     f"({time.time() - t_p:.1f}s)")
+    row_order = {"none": None, "lpa": "lpa"}.get(args.row_order)
+    if args.row_order == "auto":
+        row_order = "lpa" if (args.workload == "products" and args.partition in ("gvb", "block")) \
+            else None
+    if row_order:
+        part_name += f"; SpMM row order: {row_order} communities of each rank's block"
+    gr = GcnRun(a_hat, x, y, mask, cfg, p=p, c=c, partition=part, row_order=row_order)
     log(f"[bench] proc {w.proc}: setup {time.time() - t_setup:.1f}s")
     dims = gr.dims
     grid = gr.grid
@@ -906,9 +914,13 @@ def main():
                     help="extension: 1.5D replica reduction after the transform")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="CUDA-graph-captured epochs (auto: single process, single rank)")
-    ap.add_argument("--partition", default="auto", choices=["auto", "gvb"],
-                    help="auto: block (Reddit) / planted communities (products); "
-                         "gvb: the reference's greedy-tv -> GVB")
+    ap.add_argument("--partition", default="auto", choices=["auto", "block", "lpa", "gvb"],
+                    help="auto: block (Reddit) / lpa (products); lpa: label-propagation "
+                         "communities packed onto the parts; gvb: the reference's "
+                         "greedy-tv -> GVB")
+    ap.add_argument("--row-order", default="auto", choices=["auto", "none", "lpa"],
+                    help="SpMM processing order of each rank's rows (no effect on results); "
+                         "auto: lpa for products under a block / gvb partition")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.ranks_per_gpu is None:

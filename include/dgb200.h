@@ -66,8 +66,23 @@ int dg_spmm_plan_create(dg_spmm_plan** plan, int n_ranks,
                         const int64_t* n_rows, const int64_t* n_local, const int64_t* nnz,
                         const int64_t* const* row_ptr, const int32_t* const* col_ext,
                         const float* const* val, int32_t max_chunk, int32_t flags);
+/* As dg_spmm_plan_create, plus a processing order: row_order[r] (host, nullable; a
+ * permutation of rank r's rows) is the order in which rows are scheduled, e.g. rows
+ * grouped by graph community so the H rows gathered together stay L2-resident.  Items
+ * are bucketed by length only inside windows of ~window_nnz entries (<= 0: chosen from
+ * the graph -- DG_SPMM_WINDOW_NNZ when at least a quarter of the own-block entries are
+ * processed within one window of their row, else one global window).  The order and the
+ * window change no result: every row is still summed in its CSR storage order
+ * (bit-identical output).  dg_spmm_plan_info reports the window in info[6]. */
+#define DG_SPMM_WINDOW_NNZ (1LL << 22)
+int dg_spmm_plan_create_ordered(dg_spmm_plan** plan, int n_ranks,
+                                const int64_t* n_rows, const int64_t* n_local, const int64_t* nnz,
+                                const int64_t* const* row_ptr, const int32_t* const* col_ext,
+                                const float* const* val, int32_t max_chunk, int32_t flags,
+                                const int32_t* const* row_order, int64_t window_nnz);
 int dg_spmm_plan_destroy(dg_spmm_plan* plan);
-/* info[0]=items, [1]=split rows, [2]=chunks, [3]=total nnz, [4]=device bytes */
+/* info[0]=items, [1]=split rows, [2]=chunks, [3]=total nnz, [4]=device bytes,
+ * [5]=extended rows, [6]=length-bucketing window (entries) */
 int dg_spmm_plan_info(const dg_spmm_plan* plan, int64_t info[8]);
 /* z[r] (n_rows[r] x ld_z, device) = A_r @ [h_local[r]; h_halo[r]] (ld_h).
  * f <= ld_h, ld_h % 4 == 0, ld_z % 4 == 0.  acc: 0 = fp32 accumulate,
@@ -157,6 +172,13 @@ int dg_dense_tn(const float* H, int64_t ldh, int64_t n, int32_t K, const float* 
  *      of 16*lanes bytes.                                                  */
 int dg_diag_gather(const float* tab, int64_t ld, const int32_t* idx, int64_t n_idx,
                    int32_t lanes, int64_t groups, int32_t per_group, float* out, void* stream);
+/* Diagnostic: the same random-row gather through TMA tile::gather4 into a shared-memory
+ * ring (one producer lane per CTA, mbarrier-tracked).  Rows idx[k] (n_idx a multiple of 4,
+ * 16-B aligned) of a (rows x ld) fp32 table, box_cols floats from column col0; variant
+ * selects ring depth / rows per stage (probe.cu); ctas CTAs. */
+int dg_diag_gather_tma(const float* tab, int64_t ld, int64_t rows, int32_t col0,
+                       int32_t box_cols, const int32_t* idx, int64_t n_idx, int32_t variant,
+                       int32_t ctas, float* out, void* stream);
 
 /* ---- host preprocessing: stable O(nnz + n) transpose, bit-identical to
  *      sparse.transpose_csr (sparse.py:237-247).  Host pointers.          */

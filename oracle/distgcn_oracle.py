@@ -132,6 +132,18 @@ def local_spmm(a: Csr, h) -> np.ndarray:
     return out
 
 
+def local_spmm_fast(a: Csr, h) -> np.ndarray:
+    """The same product as `local_spmm` in float64 through scipy.sparse
+    (checker acceleration for large or long runs: the summation order
+    differs from np.add.at's by rounding at 1e-16, five orders below the
+    fp32 contract).  Used only by tests at BASELINE sizes."""
+    import scipy.sparse as sp
+    h = np.asarray(h, dtype=np.float64)
+    m = sp.csr_matrix((np.asarray(a.values, np.float64), np.asarray(a.col_idx, np.int64),
+                       np.asarray(a.row_ptr, np.int64)), shape=(a.n_rows, a.n_cols))
+    return np.asarray(m @ h)
+
+
 def serial_reference(a: Csr, h) -> np.ndarray:
     """spmm.py:249-252."""
     return local_spmm(transpose_csr(a), h)
@@ -482,9 +494,11 @@ def xent_parts(logits, labels, mask, denom):
 
 
 def serial_train(a_hat: Csr, features, labels, mask, layers, hidden, lr, epochs, seed,
-                 f_out=None, weights=None):
+                 f_out=None, weights=None, spmm=None):
     """gcn.py:135-172 + 211-227: full-batch GD on the undistributed matrix.
-    Returns (history [(loss, acc)], final weights)."""
+    Returns (history [(loss, acc)], final weights).  `spmm` (default
+    `local_spmm`) may be `local_spmm_fast` for long checker runs."""
+    local_spmm_ = local_spmm if spmm is None else spmm
     features = np.asarray(features, dtype=np.float64)
     labels = np.asarray(labels, dtype=np.int64)
     mask = np.asarray(mask, dtype=bool)
@@ -499,13 +513,13 @@ def serial_train(a_hat: Csr, features, labels, mask, layers, hidden, lr, epochs,
     for _ in range(epochs):
         hs, zs = [features], []
         for l, w in enumerate(ws):
-            z = local_spmm(fwd, hs[-1]) @ w
+            z = local_spmm_(fwd, hs[-1]) @ w
             zs.append(z)
             hs.append(np.maximum(z, 0.0) if l < last else z)
         loss_sum, g, correct = xent_parts(hs[-1], labels, mask, denom)
         ys = [None] * len(ws)
         for l in range(last, -1, -1):
-            m = local_spmm(a_hat, g)
+            m = local_spmm_(a_hat, g)
             ys[l] = hs[l].T @ m
             if l > 0:
                 g = (m @ ws[l].T) * (zs[l - 1] > 0.0)

@@ -43,6 +43,9 @@ _SIGS = {
     "dg_ipc_close": (C.c_int, [c_vp]),
     "dg_spmm_plan_create": (C.c_int, [c_vpp, C.c_int, c_i64p, c_i64p, c_i64p, c_vpp, c_vpp,
                                       c_vpp, C.c_int32, C.c_int32]),
+    "dg_spmm_plan_create_ordered": (C.c_int, [c_vpp, C.c_int, c_i64p, c_i64p, c_i64p, c_vpp,
+                                              c_vpp, c_vpp, C.c_int32, C.c_int32, c_vpp,
+                                              C.c_int64]),
     "dg_spmm_plan_destroy": (C.c_int, [c_vp]),
     "dg_spmm_plan_info": (C.c_int, [c_vp, c_i64p]),
     "dg_spmm_run": (C.c_int, [c_vp, c_vpp, c_vpp, c_vpp, C.c_int32, C.c_int64, C.c_int64,
@@ -66,6 +69,8 @@ _SIGS = {
     "dg_dense_tn_work": (C.c_int64, [C.c_int64, C.c_int32, C.c_int32]),
     "dg_dense_tn": (C.c_int, [c_vp, C.c_int64, C.c_int64, C.c_int32, c_vp, C.c_int64, C.c_int32,
                               c_vp, C.c_int64, c_vp, C.c_int64, c_vp]),
+    "dg_diag_gather_tma": (C.c_int, [c_vp, C.c_int64, C.c_int64, C.c_int32, C.c_int32, c_vp,
+                                     C.c_int64, C.c_int32, C.c_int32, c_vp, c_vp]),
     "dg_diag_gather": (C.c_int, [c_vp, C.c_int64, c_vp, C.c_int64, C.c_int32, C.c_int64,
                                  C.c_int32, c_vp, c_vp]),
     "dg_host_permute": (C.c_int, [C.c_int64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

@@ -374,10 +374,6 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
     return set_err(DG_ERR_ARG, "dense_rows: shape outside the kernel's range");
   if (n == 0) return DG_OK;
   cudaStream_t st = S(stream);
-  static const bool narrow_env = [] {
-    const char* e = std::getenv("DG_DENSE_WIDE_TILE");
-    return !e || std::atoi(e) != 0;
-  }();
 #define DG_DR4(tn, cg, bk, mb)                                                              \
   do {                                                                                      \
     constexpr int bm = 4 * 256 / (cg);                                                      \
@@ -396,16 +392,10 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
 #define DG_DR(tn, cg) DG_DR4(tn, cg, BK, 1)
   // long rows only (K >= 128): Reddit layer 1 (K=602) 0.303 -> 0.276 ms; short
   // rows (K <= 48) lose occupancy to the larger tile and run slower
-  static const int dr_var = [] {
-    const char* e = std::getenv("DG_DENSE_VAR");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (N <= 16 && ldc <= 16 && K >= 128 && narrow_env) {
+  if (N <= 16 && ldc <= 16 && K >= 128) {
     // 4 rows x 4 columns per thread, 256 rows per CTA, 16-wide k-chunks
-    // (Reddit layer 1: 0.26 -> 0.24 ms vs 32-wide; DG_DENSE_VAR sweeps)
-    if (dr_var == 1) DG_DR4(4, 4, 16, 3);
-    else if (dr_var == 3) DG_DR4(4, 4, 32, 1);
-    else DG_DR4(4, 4, 16, 2);
+    // (Reddit layer 1: 0.26 -> 0.24 ms vs 32-wide k-chunks or 3 CTAs/SM)
+    DG_DR4(4, 4, 16, 2);
   } else {
     switch (TN) {
       case 1: DG_DR(1, 16); break;
@@ -422,13 +412,7 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
 
 // the 256-wide K blocks pay only when they are mostly full: Reddit layer 1
 // (K=608) 0.29 -> 0.24 ms; K <= 100 ran up to 2.4x slower (idle k-groups)
-static bool tn4_ok(int32_t N, int32_t K) {
-  static const bool env = [] {
-    const char* e = std::getenv("DG_DENSE_TN4");
-    return !e || std::atoi(e) != 0;
-  }();
-  return N <= 16 && K >= 256 && env;
-}
+static bool tn4_ok(int32_t N, int32_t K) { return N <= 16 && K >= 256; }
 
 static int64_t tn_slices(int64_t n, int32_t K, int32_t N) {
   const int kb = tn4_ok(N, K) ? (K + 255) / 256 : (K + 63) / 64;

@@ -461,38 +461,6 @@ LaunchFn pick_launch(int G, int CPL) {
   return nullptr;
 }
 
-// Tuning overrides for sweeps (scripts/spmm_sweep.sh; unset in production,
-// read once): DG_SPMM_MINB=3|4 (CTAs/SM target of the one-chunk-per-lane
-// 256-bit kernels), DG_SPMM_E (entries per step), DG_SPMM_TWO / DG_SPMM_STG
-// (two-level fp32 sums / staged entries in the experiment grid),
-// DG_SPMM_FORCE_G + DG_SPMM_FORCE_CPL (lane shape), DG_SPMM_FORCE_V4
-// (128-bit lanes for wide rows).
-int env_int(const char* name, int dflt) {
-  const char* e = std::getenv(name);
-  return e ? std::atoi(e) : dflt;
-}
-
-LaunchFn pick_minb(int G, int MB) {
-#define DG_CASE(g, m) \
-  if (G == g && MB == m) return &launch_spmm<g, 1, true, 8, m>;
-  DG_CASE(2, 3) DG_CASE(4, 3) DG_CASE(8, 3) DG_CASE(16, 3) DG_CASE(32, 3)
-  DG_CASE(2, 4) DG_CASE(4, 4) DG_CASE(8, 4) DG_CASE(16, 4) DG_CASE(32, 4)
-#undef DG_CASE
-  return nullptr;
-}
-
-// experiment grid (DG_SPMM_E / DG_SPMM_TWO): pipeline depth, accumulation
-LaunchFn pick_exp(int G, int MB, int E, bool two) {
-#define DG_CASE(g, m, e)                                                 \
-  if (G == g && MB == m && E == e)                                       \
-    return two ? &launch_spmm<g, 1, false, 8, m, e, true>                \
-               : &launch_spmm<g, 1, true, 8, m, e, false>;
-  DG_CASE(8, 3, 2) DG_CASE(8, 4, 2) DG_CASE(16, 3, 2) DG_CASE(16, 4, 2)
-  DG_CASE(8, 3, 4) DG_CASE(8, 4, 4) DG_CASE(16, 3, 4) DG_CASE(16, 4, 4)
-#undef DG_CASE
-  return nullptr;
-}
-
 // acc == 2 (the default): one 256-bit chunk per lane, entries staged in
 // shared memory, two-level fp32 sums, 4 CTAs/SM at 2 entries per step
 // (64 registers, no spill).  Sweep (profiles/r01/spmm_sweep_stg.txt): f=602
@@ -506,17 +474,6 @@ LaunchFn pick_two(int G) {
     case 32: return &launch_spmm<32, 1, false, 8, 4, 2, true, true>;
     default: return nullptr;
   }
-}
-
-LaunchFn pick_stg(int G, int MB, int E, bool two) {
-#define DG_CASE(g, m, e)                                                 \
-  if (G == g && MB == m && E == e)                                       \
-    return two ? &launch_spmm<g, 1, false, 8, m, e, true, true>          \
-               : &launch_spmm<g, 1, true, 8, m, e, false, true>;
-  DG_CASE(8, 3, 4) DG_CASE(8, 4, 4) DG_CASE(16, 3, 4) DG_CASE(16, 4, 4)
-  DG_CASE(8, 3, 2) DG_CASE(8, 4, 2) DG_CASE(16, 3, 2) DG_CASE(16, 4, 2)
-#undef DG_CASE
-  return nullptr;
 }
 
 // Lane-group size G and chunks-per-lane CPL for `chunks` float4 chunks when
@@ -593,6 +550,7 @@ struct dg_spmm_plan {
   double* part = nullptr;
   int64_t part_cap = 0;  // doubles
   int64_t dev_bytes = 0;
+  int64_t window_nnz = 0;  // length-bucketing window used (INT64_MAX: one global window)
 };
 
 extern "C" {
@@ -611,6 +569,15 @@ int dg_spmm_plan_create(dg_spmm_plan** out, int n_ranks, const int64_t* n_rows,
                         const int64_t* n_local, const int64_t* nnz,
                         const int64_t* const* row_ptr, const int32_t* const* col_ext,
                         const float* const* val, int32_t max_chunk, int32_t flags) {
+  return dg_spmm_plan_create_ordered(out, n_ranks, n_rows, n_local, nnz, row_ptr, col_ext, val,
+                                     max_chunk, flags, nullptr, 0);
+}
+
+int dg_spmm_plan_create_ordered(dg_spmm_plan** out, int n_ranks, const int64_t* n_rows,
+                                const int64_t* n_local, const int64_t* nnz,
+                                const int64_t* const* row_ptr, const int32_t* const* col_ext,
+                                const float* const* val, int32_t max_chunk, int32_t flags,
+                                const int32_t* const* row_order, int64_t window_nnz) {
   const bool skip_empty = (flags & DG_PLAN_SKIP_EMPTY_ROWS) != 0;
   const bool dev_src = (flags & DG_PLAN_DEVICE_SRC) != 0;
   if (!out || n_ranks < 1 || n_ranks > DG_MAX_LOCAL || max_chunk < 1)
@@ -647,7 +614,20 @@ int dg_spmm_plan_create(dg_spmm_plan** out, int n_ranks, const int64_t* n_rows,
       for (int64_t k = 0; k < nnz[r]; ++k) mx = std::max(mx, col_ext[r][k]);
     }
     p->ext_rows.push_back((int64_t)mx + 1);
-    for (int64_t i = 0; i < n_rows[r]; ++i) {
+    const int32_t* ord = row_order ? row_order[r] : nullptr;
+    if (ord) {                                  // must be a permutation of the rows
+      std::vector<char> seen(n_rows[r], 0);
+      for (int64_t k = 0; k < n_rows[r]; ++k) {
+        const int32_t i = ord[k];
+        if (i < 0 || i >= n_rows[r] || seen[i]) {
+          delete p;
+          return set_err(DG_ERR_ARG, "dg_spmm_plan_create: row_order is not a permutation");
+        }
+        seen[i] = 1;
+      }
+    }
+    for (int64_t k = 0; k < n_rows[r]; ++k) {
+      const int64_t i = ord ? ord[k] : k;
       const int64_t lo = row_ptr[r][i], hi = row_ptr[r][i + 1];
       const int64_t len = hi - lo;
       if (len == 0 && skip_empty) continue;
@@ -665,11 +645,55 @@ int dg_spmm_plan_create(dg_spmm_plan** out, int n_ranks, const int64_t* n_rows,
       }
     }
   }
-  // bucket by length (descending, stable): similar trip counts per warp,
-  // heavy items first, row order kept inside a bucket for locality
-  std::stable_sort(items.begin(), items.end(), [](const Item& x, const Item& y) {
-    return bucket_of(x.len) > bucket_of(y.len);
-  });
+  // Window: explicit, or (window_nnz <= 0) chosen from the graph.  Windows
+  // pay when a row's gathers land near it in the processing order (a
+  // community order: products-shaped f=100 6.1 -> 5.5 ms); on a graph
+  // without locality (Reddit-shaped) the global heavy-first order wins
+  // (f=602 18.1 vs 18.9 ms, f=16 0.71 vs 0.81 ms).  Locality score: the
+  // share of own-block entries whose column is processed within one window
+  // of its row; >= 25% -> windows.
+  if (window_nnz <= 0) {
+    window_nnz = INT64_MAX;
+    int64_t near = 0, total_nnz = 0;
+    for (int r = 0; r < n_ranks && !dev_src; ++r) {
+      total_nnz += nnz[r];
+      if (n_local[r] != n_rows[r] || n_rows[r] == 0 || nnz[r] == 0) continue;
+      const int64_t m = n_rows[r];
+      std::vector<int64_t> pos(m);
+      for (int64_t k = 0; k < m; ++k) pos[row_order && row_order[r] ? row_order[r][k] : k] = k;
+      const int64_t reach = std::max<int64_t>(
+          1, (int64_t)((double)m * (double)DG_SPMM_WINDOW_NNZ / (double)nnz[r]));
+      for (int64_t i = 0; i < m; ++i)
+        for (int64_t e = row_ptr[r][i]; e < row_ptr[r][i + 1]; ++e) {
+          const int32_t c = col_ext[r][e];
+          if (c < m && std::llabs(pos[c] - pos[i]) <= reach) ++near;
+        }
+    }
+    if (total_nnz > 0 && near * 4 >= total_nnz) window_nnz = DG_SPMM_WINDOW_NNZ;
+  }
+  p->window_nnz = window_nnz;
+  // Items follow the row order (identity, or a locality order such as
+  // communities) in windows of ~window_nnz entries; inside a window they are
+  // bucketed by length (descending, stable): similar trip counts per warp,
+  // heavy items first.  Windows keep the rows that are in flight together
+  // -- and so the H rows they gather -- close in the row order: a global
+  // sort would spread every bucket over the whole matrix and make the whole
+  // H table the working set (products-shaped f=16: 34% L2 hit rate).
+  {
+    size_t w0 = 0;
+    int64_t acc_nnz = 0;
+    auto by_bucket = [](const Item& x, const Item& y) {
+      return bucket_of(x.len) > bucket_of(y.len);
+    };
+    for (size_t k = 0; k < items.size(); ++k) {
+      acc_nnz += items[k].len;
+      if (acc_nnz >= window_nnz || k + 1 == items.size()) {
+        std::stable_sort(items.begin() + w0, items.begin() + k + 1, by_bucket);
+        w0 = k + 1;
+        acc_nnz = 0;
+      }
+    }
+  }
   // lay the entries out in item order (the order warps stream them), each
   // item starting at an even entry (16-B aligned int4 pairs)
   std::vector<int64_t> cursor(n_ranks, 0);
@@ -786,7 +810,7 @@ int dg_spmm_plan_info(const dg_spmm_plan* p, int64_t info[8]) {
   info[3] = nnz;
   info[4] = p->dev_bytes + p->part_cap * 8;
   info[5] = ext;
-  info[6] = 0;
+  info[6] = p->window_nnz;
   info[7] = 0;
   return DG_OK;
 }
@@ -808,9 +832,8 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   // 128-bit lanes for rows of up to 48 floats: f=41/47 rows take 12 lane-
   // chunks of 16 B (3 per lane) instead of 6 x 32 B with two idle lanes of
   // eight, 1.66 vs 1.77 ms (profiles/r01/spmm_f41_lanes.txt)
-  static const int force_v4 = env_int("DG_SPMM_FORCE_V4", 0);   // sweep knob
   bool v8 = (f > 48 || (f > 8 && f <= 16 && acc == 2 && dram_table)) && ld_h % 8 == 0 &&
-            ld_z % 8 == 0 && !force_v4;
+            ld_z % 8 == 0;
   for (int r = 0; r < p->n_ranks && v8; ++r) {
     const uintptr_t al = (uintptr_t)h_local[r] | (uintptr_t)z[r] |
                          (uintptr_t)(h_halo ? h_halo[r] : nullptr);
@@ -859,9 +882,6 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   }
   int G, CPL, ns;
   choose_config(chunks, wmax, &G, &CPL, &ns);
-  static const int force_g = env_int("DG_SPMM_FORCE_G", 0);
-  static const int force_c = env_int("DG_SPMM_FORCE_CPL", 0);
-  static const int minb = env_int("DG_SPMM_MINB", 0);
   const bool two = acc == 2 && v8;
   if (two) {
     // one chunk per lane (the two-level kernel's shape): the narrowest
@@ -872,11 +892,6 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
       G = g;
       CPL = 1;
     }
-  }
-  if (force_g > 0 && force_c > 0) {
-    G = force_g;
-    CPL = force_c;
-    ns = (chunks + G * CPL - 1) / (G * CPL);
   }
   a.items = p->items;
   a.part = p->part;
@@ -891,14 +906,6 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   LaunchFn fn = v8 ? (acc ? pick_launch<true, 8>(G, CPL) : pick_launch<false, 8>(G, CPL))
                    : (acc ? pick_launch<true, 4>(G, CPL) : pick_launch<false, 4>(G, CPL));
   if (two && CPL == 1) fn = pick_two(G);
-  if (v8 && acc && CPL == 1 && minb >= 3) fn = pick_minb(G, minb);
-  static const int env_e = env_int("DG_SPMM_E", 0);
-  static const int env_two = env_int("DG_SPMM_TWO", 0);
-  if (v8 && acc && CPL == 1 && (env_e || env_two))
-    fn = pick_exp(G, minb ? minb : 3, env_e ? env_e : 4, env_two != 0);
-  static const int env_stg = env_int("DG_SPMM_STG", 0);
-  if (v8 && acc && CPL == 1 && env_stg)
-    fn = pick_stg(G, minb ? minb : 3, env_e ? env_e : 4, env_two != 0);
   if (!fn) return set_err(DG_ERR_ARG, "dg_spmm_run: no kernel for config");
   fn(a, ns, S(stream));
   DG_LAUNCHED();

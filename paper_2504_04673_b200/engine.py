@@ -35,6 +35,7 @@ __all__ = ["DevicePlan", "single_spmm", "device_gemm", "reduce_members", "pad4",
 ACC_FP64 = 1          # fp32 4-entry windows folded into fp64 accumulators
 ACC_TWO_LEVEL = 2     # two-level fp32 (<= 64 ulp of sum|terms| per item; rows >= 32 floats)
 MAX_CHUNK = 1024      # nonzeros per work item before a row is split
+SPMM_WINDOW_NNZ = 0   # entries per length-bucketing window of a plan (0: DG_SPMM_WINDOW_NNZ)
 
 
 def pad4(f: int) -> int:
@@ -80,10 +81,12 @@ def _numel(a):
     return a.numel() if isinstance(a, torch.Tensor) else a.size
 
 
-def _make_spmm_plan(rank_ops, max_chunk, flags=0):
+def _make_spmm_plan(rank_ops, max_chunk, flags=0, orders=None):
     """dg_spmm_plan over a list of RankOperand-like objects (row_ptr,
     col_ext, val, n_rows, n_local).  col_ext / val may be CUDA tensors (a
-    graph built in HBM): the entries are then laid out on the device."""
+    graph built in HBM): the entries are then laid out on the device.
+    orders: per operand, None or an int32 permutation of its rows (the
+    processing order, locality.py)."""
     lib = L.lib()
     n = len(rank_ops)
     dev = [isinstance(x.col_ext, torch.Tensor) for x in rank_ops]
@@ -95,11 +98,17 @@ def _make_spmm_plan(rank_ops, max_chunk, flags=0):
     rp = (C.c_void_p * n)(*[x.row_ptr.ctypes.data for x in rank_ops])
     ce = (C.c_void_p * n)(*[_ptr(x.col_ext) for x in rank_ops])
     va = (C.c_void_p * n)(*[_ptr(x.val) for x in rank_ops])
+    orders = [None] * n if orders is None else list(orders)
+    for o, x in zip(orders, rank_ops):
+        if o is not None and (o.dtype != np.int32 or o.size != x.n_rows):
+            raise ValueError("row order must be an int32 permutation of the rank's rows")
+    od = (C.c_void_p * n)(*[0 if o is None else o.ctypes.data for o in orders])
     h = C.c_void_p()
-    L.check(lib.dg_spmm_plan_create(C.byref(h), n, L.i64_array([x.n_rows for x in rank_ops]),
-                                    L.i64_array([x.n_local for x in rank_ops]),
-                                    L.i64_array([_numel(x.col_ext) for x in rank_ops]),
-                                    rp, ce, va, max_chunk, flags))
+    L.check(lib.dg_spmm_plan_create_ordered(
+        C.byref(h), n, L.i64_array([x.n_rows for x in rank_ops]),
+        L.i64_array([x.n_local for x in rank_ops]),
+        L.i64_array([_numel(x.col_ext) for x in rank_ops]), rp, ce, va, max_chunk, flags,
+        od if any(o is not None for o in orders) else None, SPMM_WINDOW_NNZ))
     return h
 
 
@@ -172,7 +181,7 @@ class DevicePlan:
     pass that accumulates into Z once the barrier has passed."""
 
     def __init__(self, vplan, local_ranks=None, acc=ACC_TWO_LEVEL, max_chunk=MAX_CHUNK,
-                 max_ld=None, standalone=False, parities=2):
+                 max_ld=None, standalone=False, parities=2, row_order=None):
         from .dist import world
         lib = L.lib()
         self.vplan = vplan
@@ -193,16 +202,22 @@ class DevicePlan:
         self.device = torch.device("cuda", torch.cuda.current_device())
         ro = [vplan.ranks[r] for r in self.local]
         _check_bounds(vplan, self.local)
+        # processing order of every hosted rank's rows (locality.py; no
+        # effect on any result)
+        from .locality import rank_row_order
+        self.row_order = row_order
+        orders = [rank_row_order(x, row_order, self.device) for x in ro]
         self.overlap = self.multi
         if self.overlap:
-            self._splan = _make_spmm_plan([_Part(x, False) for x in ro], max_chunk)
+            self._splan = _make_spmm_plan([_Part(x, False) for x in ro], max_chunk,
+                                          orders=orders)
             self._bplan = _make_spmm_plan([_Part(x, True) for x in ro], max_chunk,
-                                          L.DG_PLAN_SKIP_EMPTY_ROWS)
+                                          L.DG_PLAN_SKIP_EMPTY_ROWS, orders=orders)
             # high priority: the exchange's blocks are dispatched ahead of the
             # own-block SpMM's (otherwise the 10^5-block SpMM grid starves it)
             self._side = torch.cuda.Stream(device=self.device, priority=-1)
         else:
-            self._splan = _make_spmm_plan(ro, max_chunk)
+            self._splan = _make_spmm_plan(ro, max_chunk, orders=orders)
             self._bplan = None
         segs = [s for s in vplan.segments if s.src in self.li and s.count > 0]
         # blocks are dispatched roughly in segment order: rotate every

@@ -334,7 +334,7 @@ class GcnRun:
     reference where it precedes the epoch loop)."""
 
     def __init__(self, a_hat: CsrMatrix, features, labels, train_mask, cfg: TrainConfig, p=1,
-                 c=1, partition=None):
+                 c=1, partition=None, row_order=None):
         validate_variant_grid(cfg.variant, p, c)
         from .dist import world
         world().init()
@@ -380,8 +380,11 @@ class GcnRun:
         self.timer = None             # PhaseTimer for a breakdown run (bench)
         # register the device plans up front (multi-process: fixed IPC
         # buffers sized for the widest layer)
+        # row_order (locality.py): processing order of every rank's rows in
+        # the SpMM -- "lpa" groups rows by graph community; results unchanged
         from .spmm import device_plan
         for op in {id(self.dm.fwd): self.dm.fwd, id(self.dm.bwd): self.dm.bwd}.values():
+            op.row_order = row_order
             device_plan(op, grid, cfg.variant, max_ld=max(self.lds))
 
     def _inputs(self, i):

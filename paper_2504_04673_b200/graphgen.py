@@ -172,7 +172,7 @@ def _host_cumsum(t):
 
 
 def chung_lu_device(n, pairs, alpha=0.6, max_weight=None, seed=0, communities=0, p_in=0.8,
-                    return_communities=False):
+                    return_communities=False, device=None):
     """Power-law (Chung-Lu) symmetric 0/1 graph with exactly `pairs`
     undirected edges, sampled on the GPU with torch (input synthesis only).
 
@@ -180,9 +180,11 @@ def chung_lu_device(n, pairs, alpha=0.6, max_weight=None, seed=0, communities=0,
     `max_weight`, then a seeded random relabel so hubs are scattered.  With
     `communities` > 0 a fraction p_in of the edges is drawn inside hidden
     equal-size communities (planted partition, products-shaped).
-    Returns a host CsrMatrix (int64 indices, unit values)."""
+    Returns a host CsrMatrix (int64 indices, unit values).  `device`
+    (default: the current CUDA device) only decides where the draws run;
+    tests use a CPU device for small instances."""
     import torch
-    dev = torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
     g = torch.Generator(device=dev)
     g.manual_seed(int(seed))
     w = (torch.arange(n, device=dev, dtype=torch.float64) + 1.0) ** (-alpha)
@@ -242,7 +244,8 @@ def chung_lu_device(n, pairs, alpha=0.6, max_weight=None, seed=0, communities=0,
                     check=False)
     comm_host = comm.cpu().numpy() if communities else None
     del keys, rows, cols, key2, rp
-    torch.cuda.empty_cache()
+    if dev.type == "cuda":
+        torch.cuda.empty_cache()
     return (out, comm_host) if return_communities else out
 
 
@@ -288,35 +291,6 @@ def products_shaped_device(seed=0, n=2_449_029, nnz=2 * 61_859_140, communities=
     Returns (adjacency, planted community of every vertex)."""
     return chung_lu_device(n, nnz // 2, alpha=0.55, max_weight=17_481, seed=seed,
                            communities=communities, p_in=0.8, return_communities=True)
-
-
-def community_partition(communities, k):
-    """k-way partition that keeps planted communities whole, balanced by
-    vertex count (largest community first onto the lightest part) -- the
-    stand-in for the paper's METIS / GVB reordering on the products-shaped
-    graph (the reference's Python partitioners take hours at 2.4M vertices)."""
-    from .partition import Partition
-    comm = np.asarray(communities, dtype=np.int64)
-    sizes = np.bincount(comm)
-    load = np.zeros(k, dtype=np.int64)
-    part_of_comm = np.zeros(sizes.size, dtype=np.int64)
-    for c in np.argsort(-sizes, kind="stable"):
-        t = int(np.argmin(load))
-        part_of_comm[c] = t
-        load[t] += sizes[c]
-    asg = part_of_comm[comm]
-    # locality-aware layout: vertices ordered by (part, community, id), the
-    # nested ordering a METIS-style partitioner produces; parts stay
-    # contiguous, as Partition requires
-    order = np.lexsort((np.arange(comm.size), comm, asg))
-    perm = np.empty(comm.size, dtype=np.int64)
-    perm[order] = np.arange(comm.size)
-    sizes_k = np.bincount(asg, minlength=k)
-    bounds, pos = [], 0
-    for sz in sizes_k:
-        bounds.append((pos, pos + int(sz)))
-        pos += int(sz)
-    return Partition(comm.size, k, asg, perm, bounds)
 
 
 # ---------------------------------------------------------------------------

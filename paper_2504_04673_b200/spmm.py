@@ -61,7 +61,8 @@ def device_plan(op: DistOperand, grid: ProcessGrid, variant: str, max_ld=None):
         raise ValueError(f"row pitch {max_ld} exceeds this plan's registered {dp.max_ld}")
     if dp is None:
         dp = DevicePlan(build_variant_plan(op, grid, variant, local), local, max_ld=max_ld,
-                        parities=getattr(op, "parities", 2))
+                        parities=getattr(op, "parities", 2),
+                        row_order=getattr(op, "row_order", None))
         op._device[key] = dp
     return dp
 

@@ -28,23 +28,29 @@ def main():
     ap.add_argument("--slab", type=int, nargs="+", default=[0])
     ap.add_argument("--chunk", type=int, default=0)
     ap.add_argument("--ld-align", type=int, default=0)
-    ap.add_argument("--community", action="store_true",
-                    help="products: community-ordered layout (as bench.py uses)")
+    ap.add_argument("--order", default="none", choices=["none", "lpa", "lpa-part"],
+                    help="lpa: SpMM row order by label-propagation communities (plan only); "
+                         "lpa-part: relabel the graph by lpa_partition(k=1) (as bench.py)")
+    ap.add_argument("--window", type=int, default=0,
+                    help="entries per length-bucketing window of the plan (0: default)")
     ap.add_argument("--cusparse", action="store_true",
                     help="also time torch.sparse.mm (cuSPARSE) on the same matrix (comparator)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     a = bench.make_graph(args.workload)
-    if args.community and args.workload in bench._COMM:
-        from paper_2504_04673_b200.graphgen import community_partition
-        part = community_partition(bench._COMM[args.workload], 1)
+    if args.order == "lpa-part":
+        from paper_2504_04673_b200.locality import lpa_partition
+        part = lpa_partition(a, 1)
         a, _ = P.apply_partition(a, None, part)
-        print("community-ordered layout", flush=True)
+        print("lpa community-ordered layout", flush=True)
     grid = P.ProcessGrid(1, 1)
     dm = P.build_dist_matrices(a, [(0, a.n_rows)], grid)
+    import paper_2504_04673_b200.engine as E
     if args.chunk:
-        import paper_2504_04673_b200.engine as E
         E.MAX_CHUNK = args.chunk
+    E.SPMM_WINDOW_NNZ = args.window
+    if args.order == "lpa":
+        dm.fwd.row_order = "lpa"
     dp = device_plan(dm.fwd, grid, "1d-sparse")
     lib = L.lib()
     for f in args.f:

@@ -229,38 +229,3 @@ def make_partition_golden():
 
 if __name__ == "__main__":
     make_partition_golden()
-
-
-def make_cli_golden():
-    """Report files of the reference CLI (cli.py:147-196) for a few commands;
-    our CLI must write the same bytes for the volume / partition reports."""
-    import io as _io
-    import tempfile
-    sys.path.insert(0, REF)
-    from distgcn.cli import main as ref_main
-    cases = {
-        "part_gvb": ["partition", "--gen", "star-augmented", "--n", "150", "--k", "4",
-                     "--partitioner", "gvb", "--f", "8"],
-        "part_block": ["partition", "--gen", "grid", "--n", "100", "--k", "3"],
-        "spmm_15d": ["spmm-bench", "--gen", "sbm", "--n", "120", "--p", "8", "--c", "2",
-                     "--variant", "15d-sparse", "--partitioner", "gvb", "--f", "16"],
-        "spmm_1d_obl": ["spmm-bench", "--gen", "cliques", "--n", "64", "--p", "4",
-                        "--variant", "1d-oblivious", "--f", "4"],
-        "spmm_1d_rand": ["spmm-bench", "--gen", "star-augmented", "--n", "150", "--p", "4",
-                         "--variant", "1d-sparse", "--partitioner", "random", "--f", "3"],
-    }
-    out = {}
-    for name, argv in cases.items():
-        with tempfile.TemporaryDirectory() as d:
-            rc = ref_main(argv + ["--out-dir", d])
-            assert rc == 0, name
-            for fn in sorted(os.listdir(d)):
-                out[f"{name}__{fn}"] = np.frombuffer(open(os.path.join(d, fn), "rb").read(),
-                                                     dtype=np.uint8)
-        out[f"{name}__argv"] = np.array(argv)
-    out["cases"] = np.array(list(cases))
-    np.savez_compressed(os.path.join(HERE, "cli_golden.npz"), **out)
-
-
-if __name__ == "__main__":
-    make_cli_golden()

@@ -1,0 +1,174 @@
+"""GCN parity at the BASELINE configurations, against the CPU
+oracle in float64.
+
+* Config 1 (R-MAT-14, `TrainConfig(layers=3, hidden=16, lr=0.01, seed=1)`):
+  100 epochs at p=4 `1d-sparse` / `1d-oblivious` and p=8, c=2 `15d-sparse`
+  -- every epoch's loss within rtol 1e-5 of `oracle.serial_train`
+  (reference gcn.py:211-227, pinned by reference tests/test_gcn.py:136-150),
+  the final weights within the fp32 contract.
+* Configs 2 and 3 at FULL size (Reddit-shaped 115M nonzeros, f=602;
+  products-shaped 126M nonzeros, f=100): one epoch's loss and every weight
+  gradient Y_l = H_l^T M_l (gcn.py:280) against an independent float64 host
+  computation (scipy.sparse).  The host side evaluates the same function
+  transform-first, A (H W) = (A H) W, which keeps the float64 reference to
+  seconds; the reassociation changes float64 results at 1e-15, far below the
+  tolerance.  Config 4's 1.5D c=2 (p=8 ranks, grid 4x2) runs on the
+  products graph.
+
+Gradients are read back through the SGD step with a large learning rate:
+W1 = W0 - lr Y, so Y = (W0 - W1) / lr with an fp32 rounding error of
+ulp(lr |Y|) / lr, relative 6e-8.
+
+Tolerance (written here): loss rtol 1e-5; Y elementwise
+|Y_gpu - Y_ref| <= 1e-5 * Ymag + 1e-30, Ymag = |H|^T (|A^T| |G|) -- the sum
+of |terms| of the whole chain that produces Y -- so reduction-order
+differences of fp32 sums are allowed and nothing else."""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2504_04673_b200 as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+import distgcn_oracle as O  # noqa: E402  (checker only)
+
+pytestmark = pytest.mark.gpu
+
+
+# ---------------------------------------------------------------------------
+# config 1: 100 epochs
+# ---------------------------------------------------------------------------
+
+@pytest.fixture(scope="module")
+def config1():
+    from paper_2504_04673_b200.graphgen import rmat
+    a = P.gcn_normalize(rmat(14, 16, 0))
+    a.values = a.values.astype(np.float32).astype(np.float64)
+    n = a.n_rows
+    x = np.random.default_rng(1).standard_normal((n, 16)).astype(np.float32)
+    y = np.random.default_rng(2).integers(0, 16, n)
+    mask = np.ones(n, bool)
+    oa = O.Csr(n, n, a.row_ptr, a.col_idx, a.values)
+    w0 = [w.astype(np.float32).astype(np.float64) for w in O.init_weights(1, 3, 16, 16, 16)]
+    hist, ws = O.serial_train(oa, x.astype(np.float64), y, mask, 3, 16, 0.01, 100, 1,
+                              weights=w0, spmm=O.local_spmm_fast)
+    return a, x, y, mask, np.array([h[0] for h in hist]), ws
+
+
+@pytest.mark.parametrize("variant,p,c", [("1d-sparse", 4, 1), ("1d-oblivious", 4, 1),
+                                         ("15d-sparse", 8, 2)])
+def test_config1_100_epochs_match_oracle(config1, variant, p, c):
+    a, x, y, mask, ref_loss, ref_w = config1
+    cfg = P.TrainConfig(layers=3, hidden=16, lr=0.01, epochs=100, seed=1, variant=variant)
+    res = P.train(a, x, y, mask, cfg, p=p, c=c)
+    assert res.losses.shape == (100,)
+    assert np.allclose(res.losses, ref_loss, rtol=1e-5, atol=0), \
+        float(np.max(np.abs(res.losses / ref_loss - 1)))
+    # the loss moves by ~1e-3 over the run: the check sees training, not a constant
+    assert abs(ref_loss[-1] - ref_loss[0]) > 100 * 1e-5 * abs(ref_loss[0])
+    for wg, wr in zip(res.weights, ref_w):
+        # 100 fp32 SGD steps, each within the 1e-5 contract of its f64 step
+        assert np.max(np.abs(wg - wr)) <= 1e-5 * np.max(np.abs(wr)) * 10, \
+            float(np.max(np.abs(wg - wr)) / np.max(np.abs(wr)))
+    # replication: every rank holds the same weights, bit for bit
+    for per_rank in res.weights_per_rank[1:]:
+        for w0_, wr_ in zip(res.weights_per_rank[0], per_rank):
+            assert np.array_equal(w0_, wr_)
+
+
+# ---------------------------------------------------------------------------
+# configs 2 / 3 (/ 4): one full-size epoch
+# ---------------------------------------------------------------------------
+
+def _xent(logits, labels, denom):
+    shift = logits - logits.max(axis=1, keepdims=True)
+    e = np.exp(shift)
+    s = e.sum(axis=1, keepdims=True)
+    rows = np.arange(logits.shape[0])
+    loss = float((np.log(s[:, 0]) - shift[rows, labels]).sum()) / denom
+    g = e / s
+    g[rows, labels] -= 1.0
+    return loss, g / denom
+
+
+def _reference_epoch(a, x, y, w0):
+    """One epoch of gcn.py:258-286 (serial, full mask) in float64 with
+    scipy: returns (loss, [Y_l], [Ymag_l])."""
+    import scipy.sparse as sp
+    n = a.n_rows
+    m = sp.csr_matrix((a.values, a.col_idx, a.row_ptr), shape=(n, n))
+    mt = m.T.tocsr()                     # forward operand A^T (spmm.py:114)
+    am, amt = abs(m), abs(mt)
+    hs, zs = [x.astype(np.float64)], []
+    last = len(w0) - 1
+    for l, w in enumerate(w0):
+        z = mt @ (hs[-1] @ w)            # = (A^T H) W, transform-first in f64
+        zs.append(z)
+        hs.append(np.maximum(z, 0.0) if l < last else z)
+    loss, g = _xent(hs[-1], y, n)
+    ys, mags = [None] * len(w0), [None] * len(w0)
+    for l in range(last, -1, -1):
+        mm = m @ g                       # backward operand A (gcn.py:279)
+        ys[l] = hs[l].T @ mm
+        mags[l] = np.abs(hs[l]).T @ (am @ np.abs(g))
+        if l > 0:
+            g = (mm @ w0[l].T) * (zs[l - 1] > 0.0)
+    return loss, ys, mags
+
+
+def _full_epoch_check(a, x, y, wl, p, c, variant, partition=None, lr=100.0):
+    from paper_2504_04673_b200.gcn import GcnRun
+    n = a.n_rows
+    mask = np.ones(n, bool)
+    cfg = P.TrainConfig(layers=wl["layers"], hidden=wl["hidden"], lr=lr, epochs=1, seed=1,
+                        variant=variant)
+    gr = GcnRun(a, x, y, mask, cfg, p=p, c=c, partition=partition)
+    w_init = [w[:d0, :d1].double().cpu().numpy()
+              for w, d0, d1 in zip(gr.w0, gr.dims[:-1], gr.dims[1:])]
+    run = gr.run_lockstep() if p > 1 else gr.run()
+    res = gr.result(run)
+    gr.close()
+    del gr
+    torch.cuda.empty_cache()
+    loss_ref, ys, mags = _reference_epoch(a, x, y, w_init)
+    assert abs(res.losses[0] - loss_ref) <= 1e-5 * abs(loss_ref), (res.losses[0], loss_ref)
+    for l, (w1, yr, mg) in enumerate(zip(res.weights, ys, mags)):
+        yg = (w_init[l] - w1.astype(np.float64)) / lr
+        bound = 1e-5 * mg + 6e-8 * np.abs(yr).max() + 1e-30
+        bad = np.abs(yg - yr) > bound
+        assert not bad.any(), (l, float(np.max(np.abs(yg - yr) / (mg + 1e-30))))
+        print(f"[{variant} p={p} c={c}] Y_{l}: max |err| / max |Y| = "
+              f"{np.abs(yg - yr).max() / np.abs(yr).max():.2e}, max err / Ymag = "
+              f"{np.max(np.abs(yg - yr) / (mg + 1e-30)):.2e}")
+
+
+def _shaped(name):
+    sys.path.insert(0, ROOT)
+    import bench
+    a = bench.make_graph(name)
+    wl = bench.WORKLOADS[name]
+    x, y, _ = bench.make_inputs(wl, a.n_rows)
+    return a, x, y, wl
+
+
+@pytest.mark.timeout(2400)
+def test_config2_reddit_full_epoch_matches_fp64():
+    torch.cuda.set_device(0)
+    a, x, y, wl = _shaped("reddit")
+    _full_epoch_check(a, x, y, wl, 1, 1, "1d-sparse")
+    _full_epoch_check(a, x, y, wl, 4, 1, "1d-oblivious")
+
+
+@pytest.mark.timeout(2400)
+def test_config3_4_products_full_epoch_matches_fp64():
+    torch.cuda.set_device(0)
+    from paper_2504_04673_b200.locality import lpa_partition
+    a, x, y, wl = _shaped("products")
+    _full_epoch_check(a, x, y, wl, 1, 1, "1d-sparse")
+    part = lpa_partition(a, 4)
+    _full_epoch_check(a, x, y, wl, 8, 2, "15d-sparse", partition=part)
