@@ -81,6 +81,9 @@ int dg_spmm_plan_create_ordered(dg_spmm_plan** plan, int n_ranks,
                                 const float* const* val, int32_t max_chunk, int32_t flags,
                                 const int32_t* const* row_order, int64_t window_nnz);
 int dg_spmm_plan_destroy(dg_spmm_plan* plan);
+/* Size the plan's fp64 split-row partial buffer for row pitches up to ld_max, so that
+ * dg_spmm_run never allocates (it refuses to grow the buffer inside a stream capture). */
+int dg_spmm_plan_reserve(dg_spmm_plan* plan, int64_t ld_max);
 /* info[0]=items, [1]=split rows, [2]=chunks, [3]=total nnz, [4]=device bytes,
  * [5]=extended rows, [6]=length-bucketing window (entries) */
 int dg_spmm_plan_info(const dg_spmm_plan* plan, int64_t info[8]);

@@ -47,6 +47,7 @@ _SIGS = {
                                               c_vpp, c_vpp, C.c_int32, C.c_int32, c_vpp,
                                               C.c_int64]),
     "dg_spmm_plan_destroy": (C.c_int, [c_vp]),
+    "dg_spmm_plan_reserve": (C.c_int, [c_vp, C.c_int64]),
     "dg_spmm_plan_info": (C.c_int, [c_vp, c_i64p]),
     "dg_spmm_run": (C.c_int, [c_vp, c_vpp, c_vpp, c_vpp, C.c_int32, C.c_int64, C.c_int64,
                               C.c_int32, C.c_int32, C.c_int32, c_vp]),

@@ -20,6 +20,7 @@
 // (fp64) -- deterministic, unlike split-K with atomics.
 
 #include "common.cuh"
+#include "tma.cuh"
 
 #include <cstdlib>
 
@@ -124,6 +125,135 @@ __global__ void __launch_bounds__(256, MB) dense_rows_kernel(
       if (Zmask && j < N && !(Zmask[gr * ldm + j] > 0.f)) v = 0.f;
       C[gr * ldc + j] = v;
       if (Crelu) Crelu[gr * ldc + j] = fmaxf(v, 0.f);
+    }
+  }
+}
+
+// TMA-fed form of dense_rows (the default for N <= 64).  Persistent CTAs,
+// one producer warp + 8 consumer warps.  The producer streams 128-row x
+// 32-column tiles of A (16 KB, 128-byte swizzle) into a 4-deep shared-memory
+// ring with cp.async.bulk.tensor (mbarrier completion): 64 KB of A in
+// flight per CTA without a register held, which the register-staged kernel
+// above could not reach (ncu: 24% warps active, ~36% of HBM).  B (K x NP)
+// sits in shared memory for the whole kernel.  Consumer thread tile: rows
+// rg and rg + 64 of the 128-row tile x NP/4 columns; per k-quad two
+// swizzled 16-B A loads (8 consecutive rows hit 8 distinct bank groups)
+// and NP/16 16-B B loads (broadcast) feed 2 * NP FMAs.
+constexpr int TR_BM = 128;          // rows per tile
+constexpr int TR_BK = 32;           // columns per stage (one 128-byte swizzle span)
+constexpr int TR_STAGES = 4;
+constexpr int TR_STAGE_BYTES = TR_BM * TR_BK * 4;
+
+template <int NP>
+__global__ void __launch_bounds__(288, 2) dense_rows_tma_kernel(
+    const __grid_constant__ CUtensorMap amap, int64_t n, int K, const float* __restrict__ B,
+    int64_t ldb, int N, int transB, float* __restrict__ C, int64_t ldc,
+    float* __restrict__ Crelu, const float* __restrict__ Zmask, int64_t ldm) {
+  constexpr int TN = NP / 4;                         // columns per thread
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B alignment of the ring (128-byte swizzle atoms)
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* ring = base;
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + TR_STAGES * TR_STAGE_BYTES);
+  uint64_t* empty = full + TR_STAGES;
+  float* Bs = reinterpret_cast<float*>(empty + TR_STAGES);   // K_pad x NP
+  const int nk = (K + TR_BK - 1) / TR_BK;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < nk * TR_BK * NP; i += blockDim.x) {
+    const int k = i / NP, j = i % NP;
+    float b = 0.f;
+    if (k < K && j < N) b = transB ? B[(int64_t)j * ldb + k] : B[(int64_t)k * ldb + j];
+    Bs[i] = b;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < TR_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int64_t ntiles = (n + TR_BM - 1) / TR_BM;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (warp == 8) {                                   // producer
+    if (lane == 0) {
+      int64_t it = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int slot = (int)(it % TR_STAGES);
+          if (it >= TR_STAGES) mbar_wait(&empty[slot], (uint32_t)(((it / TR_STAGES) - 1) & 1));
+          mbar_arrive_expect_tx(&full[slot], TR_STAGE_BYTES);
+          tma_load_2d(ring + (size_t)slot * TR_STAGE_BYTES, &amap, &full[slot], kc * TR_BK,
+                      (int32_t)(t * TR_BM));
+        }
+    }
+    return;
+  }
+  const int cg = tid & 3;                            // columns cg*TN .. cg*TN+TN-1
+  const int rg = tid >> 2;                           // rows rg, rg + 64 of the tile
+  int64_t it = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    float acc[2][TN];
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < TN; ++c) acc[r][c] = 0.f;
+    for (int kc = 0; kc < nk; ++kc, ++it) {
+      const int slot = (int)(it % TR_STAGES);
+      mbar_wait(&full[slot], (uint32_t)((it / TR_STAGES) & 1));
+      const unsigned char* st = ring + (size_t)slot * TR_STAGE_BYTES;
+      const float* bk = Bs + (size_t)kc * TR_BK * NP + cg * TN;
+#pragma unroll
+      for (int q = 0; q < TR_BK / 4; ++q) {
+        float4 a[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int row = rg + 64 * r;
+          a[r] = *reinterpret_cast<const float4*>(st + row * 128 + ((q ^ (row & 7)) << 4));
+        }
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          float b[TN];
+#pragma unroll
+          for (int c4 = 0; c4 < TN / 4; ++c4) {
+            const float4 v = *reinterpret_cast<const float4*>(bk + (4 * q + kk) * NP + 4 * c4);
+            b[4 * c4] = v.x;
+            b[4 * c4 + 1] = v.y;
+            b[4 * c4 + 2] = v.z;
+            b[4 * c4 + 3] = v.w;
+          }
+          const float a0 = kk == 0 ? a[0].x : kk == 1 ? a[0].y : kk == 2 ? a[0].z : a[0].w;
+          const float a1 = kk == 0 ? a[1].x : kk == 1 ? a[1].y : kk == 2 ? a[1].z : a[1].w;
+#pragma unroll
+          for (int c = 0; c < TN; ++c) {
+            acc[0][c] = fmaf(a0, b[c], acc[0][c]);
+            acc[1][c] = fmaf(a1, b[c], acc[1][c]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int64_t gr = t * TR_BM + rg + 64 * r;
+      if (gr >= n) continue;
+#pragma unroll
+      for (int c4 = 0; c4 < TN / 4; ++c4) {
+        const int j = cg * TN + 4 * c4;
+        if (j >= ldc) continue;
+        float v[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          v[e] = acc[r][4 * c4 + e];
+          if (Zmask && j + e < N && !(Zmask[gr * ldm + j + e] > 0.f)) v[e] = 0.f;
+        }
+        *reinterpret_cast<float4*>(C + gr * ldc + j) = make_float4(v[0], v[1], v[2], v[3]);
+        if (Crelu)
+          *reinterpret_cast<float4*>(Crelu + gr * ldc + j) =
+              make_float4(fmaxf(v[0], 0.f), fmaxf(v[1], 0.f), fmaxf(v[2], 0.f), fmaxf(v[3], 0.f));
+      }
     }
   }
 }
@@ -340,6 +470,117 @@ __global__ void __launch_bounds__(256, 2) dense_tn4_kernel(
   }
 }
 
+// TMA-fed form of dense_tn (the default for N <= 64).  CTA (slice, K block):
+// a producer lane streams RC-row tiles of H (KB columns from k0) and of M
+// (NP columns) into a 3-deep shared-memory ring; consumer thread (kq, nq, rs)
+// owns the 4 x 4 outputs k0+4kq.., 4nq.. over rows rs, rs+RS, ... of every
+// tile (fp32 per tile, folded into fp64), then the RS row subsets are summed
+// in fixed order through shared memory -- deterministic, like the slice sum
+// that follows.
+constexpr int TT_STAGES = 3;
+
+struct TnGeom {
+  int KB, NP, RC, RS;
+};
+
+__global__ void __launch_bounds__(288, 2) dense_tn_tma_kernel(
+    const __grid_constant__ CUtensorMap hmap, const __grid_constant__ CUtensorMap mmap,
+    int K, const TnGeom g, int64_t rows_per, int64_t n, double* __restrict__ work) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int KB = g.KB, NP = g.NP, RC = g.RC, RS = g.RS;
+  const int hfl = RC * KB, mfl = RC * NP;              // floats per stage
+  float* ring = reinterpret_cast<float*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)TT_STAGES * (hfl + mfl));
+  uint64_t* empty = full + TT_STAGES;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < TT_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const int k0 = blockIdx.y * KB;
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per;
+  const int64_t r_end = min(n, r_begin + rows_per);
+  const int64_t nst = r_end > r_begin ? (r_end - r_begin + RC - 1) / RC : 0;
+  const int warp = tid >> 5, lane = tid & 31;
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int64_t s = 0; s < nst; ++s) {
+        const int slot = (int)(s % TT_STAGES);
+        if (s >= TT_STAGES) mbar_wait(&empty[slot], (uint32_t)(((s / TT_STAGES) - 1) & 1));
+        mbar_arrive_expect_tx(&full[slot], (uint32_t)(hfl + mfl) * 4);
+        float* st = ring + (size_t)slot * (hfl + mfl);
+        const int32_t r0 = (int32_t)(r_begin + s * RC);
+        tma_load_2d(st, &hmap, &full[slot], k0, r0);
+        tma_load_2d(st + hfl, &mmap, &full[slot], 0, r0);
+      }
+    }
+    return;
+  }
+  const int nkq = KB / 4, nnq = NP / 4;
+  const int kq = tid % nkq, nq = (tid / nkq) % nnq, rs = tid / (nkq * nnq);
+  const bool active = rs < RS;
+  float part[4][4];
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      part[i][c] = 0.f;
+      acc[i][c] = 0.0;
+    }
+  for (int64_t s = 0; s < nst; ++s) {
+    const int slot = (int)(s % TT_STAGES);
+    mbar_wait(&full[slot], (uint32_t)((s / TT_STAGES) & 1));
+    const float* hs = ring + (size_t)slot * (hfl + mfl);
+    const float* ms = hs + hfl;
+    if (active) {
+#pragma unroll 4
+      for (int rr = rs; rr < RC; rr += RS) {
+        const float4 h = *reinterpret_cast<const float4*>(hs + rr * KB + 4 * kq);
+        const float4 m = *reinterpret_cast<const float4*>(ms + rr * NP + 4 * nq);
+        const float hh[4] = {h.x, h.y, h.z, h.w};
+        const float mm[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) part[i][c] = fmaf(hh[i], mm[c], part[i][c]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[i][c] += (double)part[i][c];
+          part[i][c] = 0.f;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[slot]);
+  }
+  // sum the RS row subsets in order (ring reused once every stage is consumed)
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  double* red = reinterpret_cast<double*>(ring);       // [RS][KB][NP]
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        red[((size_t)rs * KB + 4 * kq + i) * NP + 4 * nq + c] = acc[i][c];
+  }
+  asm volatile("bar.sync 1, 256;" ::: "memory");
+  double* wp = work + (size_t)blockIdx.x * K * NP;
+  for (int e = tid; e < KB * NP; e += 256) {
+    const int k = k0 + e / NP;
+    if (k >= K) continue;
+    double v = 0.0;
+    for (int r = 0; r < RS; ++r) v += red[(size_t)r * KB * NP + e];
+    wp[(size_t)k * NP + e % NP] = v;
+  }
+}
+
 // One warp per output element: lane l sums slices l, l+32, ... in order,
 // then a fixed xor tree -- deterministic, and the slices' partials are read
 // 32 at a time instead of one dependent load per slice.
@@ -365,6 +606,9 @@ int nblk_of(int N) { return N > 64 ? (N + 63) / 64 : 1; }
 
 extern "C" {
 
+// 1: the register-staged kernels only (A/B comparison in scripts/dense_probe.py)
+int dg_dense_legacy = 0;
+
 int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float* B, int64_t ldb,
                   int32_t N, int32_t transB, float* C, int64_t ldc, float* C_relu,
                   const float* z_mask, int64_t ld_mask, void* stream) {
@@ -374,6 +618,41 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
     return set_err(DG_ERR_ARG, "dense_rows: shape outside the kernel's range");
   if (n == 0) return DG_OK;
   cudaStream_t st = S(stream);
+  // TMA-fed kernel: N <= 64, 16-B aligned row pitches (ldc: vector stores)
+  if (!dg_dense_legacy && (ldc & 3) == 0 && ((uintptr_t)C & 15) == 0 &&
+      (!C_relu || ((uintptr_t)C_relu & 15) == 0)) {
+    const int NP = (N + 15) / 16 * 16;
+    const int nk = (K + TR_BK - 1) / TR_BK;
+    if (ldc <= NP && (size_t)nk * TR_BK * NP * 4 <= 64 * 1024) {
+      CUtensorMap amap;
+      int rc = dg::make_tensor_map_2d_swz128(&amap, A, n, lda, K, TR_BK, TR_BM);
+      if (rc) return rc;
+      const size_t smem = 1024 + (size_t)TR_STAGES * TR_STAGE_BYTES + 2 * TR_STAGES * 8 +
+                          (size_t)nk * TR_BK * NP * 4;
+      const int64_t ntiles = (n + TR_BM - 1) / TR_BM;
+      const unsigned grid = (unsigned)std::min<int64_t>(ntiles, 2 * 148);
+#define DG_TR(np)                                                                           \
+  do {                                                                                      \
+    static bool attr = false;                                                               \
+    if (!attr) {                                                                            \
+      DG_CK(cudaFuncSetAttribute(dense_rows_tma_kernel<np>,                                 \
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024)); \
+      attr = true;                                                                          \
+    }                                                                                       \
+    dense_rows_tma_kernel<np><<<grid, 288, smem, st>>>(amap, n, K, B, ldb, N, transB, C, ldc, \
+                                                        C_relu, z_mask, ld_mask);           \
+  } while (0)
+      switch (NP) {
+        case 16: DG_TR(16); break;
+        case 32: DG_TR(32); break;
+        case 48: DG_TR(48); break;
+        default: DG_TR(64); break;
+      }
+#undef DG_TR
+      DG_LAUNCHED();
+      return DG_OK;
+    }
+  }
 #define DG_DR4(tn, cg, bk, mb)                                                              \
   do {                                                                                      \
     constexpr int bm = 4 * 256 / (cg);                                                      \
@@ -414,6 +693,28 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
 // (K=608) 0.29 -> 0.24 ms; K <= 100 ran up to 2.4x slower (idle k-groups)
 static bool tn4_ok(int32_t N, int32_t K) { return N <= 16 && K >= 256; }
 
+// geometry of the TMA-fed dense_tn: K blocks of <= 256 columns, rows per
+// stage sized for ~32 KB of H + M, RS row subsets filling 256 threads
+static bool tn_tma_geom(int32_t K, int32_t N, TnGeom* g, int* kblocks) {
+  if (N > 64 || K % 4) return false;
+  g->NP = (N + 15) / 16 * 16;
+  g->KB = K <= 256 ? K : 256;
+  *kblocks = (K + g->KB - 1) / g->KB;
+  const int per_row = g->KB + g->NP;
+  int rc = 32768 / (per_row * 4);
+  rc = std::max(8, std::min(256, rc / 8 * 8));
+  g->RC = rc;
+  const int th = (g->KB / 4) * (g->NP / 4);
+  if (th > 256) return false;
+  g->RS = std::max(1, std::min(256 / th, rc));
+  return true;
+}
+
+static int64_t tn_tma_slices(int64_t n, int kblocks, int RC) {
+  const int64_t want = std::max<int64_t>(1, (4 * 148) / kblocks);
+  return std::max<int64_t>(1, std::min<int64_t>(want, (n + RC - 1) / RC));
+}
+
 static int64_t tn_slices(int64_t n, int32_t K, int32_t N) {
   const int kb = tn4_ok(N, K) ? (K + 255) / 256 : (K + 63) / 64;
   int64_t slices = std::max<int64_t>(1, (4 * 148) / kb);
@@ -421,7 +722,11 @@ static int64_t tn_slices(int64_t n, int32_t K, int32_t N) {
 }
 
 int64_t dg_dense_tn_work(int64_t n, int32_t K, int32_t N) {
-  return tn_slices(n, K, N) * (int64_t)K * 16 * tn_of(N) * nblk_of(N);
+  TnGeom g;
+  int kb;
+  const int64_t legacy = tn_slices(n, K, N) * (int64_t)K * 16 * tn_of(N) * nblk_of(N);
+  if (!tn_tma_geom(K, N, &g, &kb)) return legacy;
+  return std::max(legacy, tn_tma_slices(n, kb, g.RC) * (int64_t)K * g.NP);
 }
 
 int dg_dense_tn(const float* H, int64_t ldh, int64_t n, int32_t K, const float* M, int64_t ldm,
@@ -433,6 +738,40 @@ int dg_dense_tn(const float* H, int64_t ldh, int64_t n, int32_t K, const float* 
   if (n < 0 || K < 1 || N < 1 || N > 256 || (ldh & 3) || ((uintptr_t)H & 15) || ldy > NPT ||
       ldy < N)
     return set_err(DG_ERR_ARG, "dense_tn: shape outside the kernel's range");
+  cudaStream_t st0 = S(stream);
+  TnGeom g;
+  int kbt;
+  if (!dg_dense_legacy && tn_tma_geom(K, N, &g, &kbt) && (ldm & 3) == 0 &&
+      ((uintptr_t)M & 15) == 0 && ldy <= g.NP) {
+    const int64_t slices = tn_tma_slices(n, kbt, g.RC);
+    if (work_len < slices * (int64_t)K * g.NP)
+      return set_err(DG_ERR_ARG, "dense_tn: work buffer too small");
+    int64_t rows_per = (n + slices - 1) / slices;
+    rows_per = (rows_per + g.RC - 1) / g.RC * g.RC;          // whole stages per slice
+    CUtensorMap hmap, mmap;
+    int rc = dg::make_tensor_map_2d(&hmap, H, n, ldh, K, g.KB, g.RC, true);
+    if (rc) return rc;
+    rc = dg::make_tensor_map_2d(&mmap, M, n, ldm, N, g.NP, g.RC, true);
+    if (rc) return rc;
+    const size_t ring = (size_t)TT_STAGES * g.RC * (g.KB + g.NP) * 4;
+    const size_t red = (size_t)g.RS * g.KB * g.NP * 8;
+    const size_t smem = std::max(ring, red) + 2 * TT_STAGES * 8 + 16;
+    static bool attr = false;
+    if (!attr) {
+      DG_CK(cudaFuncSetAttribute(dense_tn_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 200 * 1024));
+      attr = true;
+    }
+    if (smem > 200 * 1024) return set_err(DG_ERR_ARG, "dense_tn: shared memory");
+    dense_tn_tma_kernel<<<dim3((unsigned)slices, (unsigned)kbt), 288, smem, st0>>>(
+        hmap, mmap, K, g, rows_per, n, work);
+    DG_LAUNCHED();
+    const int total = K * g.NP;
+    dense_tn_reduce_kernel<<<(unsigned)std::min(4096, (total + 7) / 8), 256, 0, st0>>>(
+        work, (int)slices, K, g.NP, N, Y, ldy);
+    DG_LAUNCHED();
+    return DG_OK;
+  }
   const bool t4 = tn4_ok(N, K);
   const int kb = t4 ? (K + 255) / 256 : (K + 63) / 64;
   const int64_t slices = tn_slices(n, K, N);

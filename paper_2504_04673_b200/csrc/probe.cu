@@ -30,8 +30,24 @@ EncodeFn encode_fn() {
 }
 }  // namespace
 
+static int encode_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t ld, int64_t cols,
+                     int box_cols, int box_rows, bool l2_promote_256, CUtensorMapSwizzle swz);
+
 int make_tensor_map_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t ld,
                        int64_t cols, int box_cols, int box_rows, bool l2_promote_256) {
+  return encode_2d(map, base, rows, ld, cols, box_cols, box_rows, l2_promote_256,
+                   CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+int make_tensor_map_2d_swz128(CUtensorMap* map, const void* base, int64_t rows, int64_t ld,
+                              int64_t cols, int box_cols, int box_rows) {
+  if (box_cols * 4 != 128) return set_err(DG_ERR_ARG, "128-byte swizzle needs 128-byte boxes");
+  return encode_2d(map, base, rows, ld, cols, box_cols, box_rows, true,
+                   CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+static int encode_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t ld, int64_t cols,
+                     int box_cols, int box_rows, bool l2_promote_256, CUtensorMapSwizzle swz) {
   EncodeFn fn = encode_fn();
   if (!fn) return set_err(DG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   if (((uintptr_t)base & 15) || (ld * 4) % 16 || box_cols < 1 || box_cols > 256 ||
@@ -42,8 +58,7 @@ int make_tensor_map_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t
   const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
-                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        CU_TENSOR_MAP_SWIZZLE_NONE,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                         l2_promote_256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
                                        : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -82,18 +97,21 @@ __global__ void __launch_bounds__(32 * (CW + 1)) gather_tma_probe_kernel(
   const int64_t s1 = min((int64_t)(blockIdx.x + 1) * per, n_quads / G4);
   const int64_t nst = max((int64_t)0, s1 - s0);
   if (warp == 0) {
-    if (lane == 0) {
-      for (int64_t s = 0; s < nst; ++s) {
-        const int slot = (int)(s % STAGES);
-        if (s >= STAGES) mbar_wait(&empty[slot], (uint32_t)(((s / STAGES) - 1) & 1));
-        mbar_arrive_expect_tx(&full[slot], STAGE_FLOATS * 4);
-        float* dst = ring + (size_t)slot * STAGE_FLOATS;
-#pragma unroll
-        for (int g = 0; g < G4; ++g) {
-          const int4 r = __ldg(idx4 + (s0 + s) * G4 + g);
-          tma_gather4(dst + g * 4 * BOX, &map, &full[slot], c0, r.x, r.y, r.z, r.w);
-        }
-      }
+    // lanes 0..G4-1 each issue one gather4 per stage (TMA issue from
+    // several lanes); every lane's indices are loaded one stage ahead so no
+    // issue waits on an index load
+    int4 nxt = make_int4(0, 0, 0, 0);
+    if (nst > 0 && lane < G4) nxt = __ldg(idx4 + s0 * G4 + lane);
+    for (int64_t s = 0; s < nst; ++s) {
+      const int slot = (int)(s % STAGES);
+      if (s >= STAGES) mbar_wait(&empty[slot], (uint32_t)(((s / STAGES) - 1) & 1));
+      if (lane == 0) mbar_arrive_expect_tx(&full[slot], STAGE_FLOATS * 4);
+      __syncwarp();
+      const int4 r = nxt;
+      if (s + 1 < nst && lane < G4) nxt = __ldg(idx4 + (s0 + s + 1) * G4 + lane);
+      if (lane < G4)
+        tma_gather4(ring + (size_t)slot * STAGE_FLOATS + lane * 4 * BOX, &map, &full[slot], c0,
+                    r.x, r.y, r.z, r.w);
     }
     return;
   }

@@ -799,6 +799,18 @@ int dg_spmm_plan_create_ordered(dg_spmm_plan** out, int n_ranks, const int64_t* 
   return DG_OK;
 }
 
+int dg_spmm_plan_reserve(dg_spmm_plan* p, int64_t ld_max) {
+  if (!p || ld_max < 0) return set_err(DG_ERR_ARG, "dg_spmm_plan_reserve: bad args");
+  const int64_t need = p->n_slots * ld_max;
+  if (need <= p->part_cap) return DG_OK;
+  if (p->part) DG_CK(cudaFree(p->part));
+  p->part = nullptr;
+  p->part_cap = 0;
+  DG_CK(cudaMalloc(&p->part, need * sizeof(double)));
+  p->part_cap = need;
+  return DG_OK;
+}
+
 int dg_spmm_plan_info(const dg_spmm_plan* p, int64_t info[8]) {
   if (!p) return set_err(DG_ERR_ARG, "null plan");
   int64_t nnz = 0, ext = 0;
@@ -858,11 +870,15 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   if (p->n_slots) {
     const int64_t need = p->n_slots * ld_h;
     if (need > p->part_cap) {
-      if (p->part) cudaFree(p->part);
-      p->part = nullptr;
-      p->part_cap = 0;
-      DG_CK(cudaMalloc(&p->part, need * sizeof(double)));
-      p->part_cap = need;
+      // growing frees and allocates (a device-wide sync): never inside a
+      // stream capture -- plans used by captured epochs are reserved up
+      // front (dg_spmm_plan_reserve) for the widest pitch of the run
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      DG_CK(cudaStreamIsCapturing(S(stream), &cs));
+      if (cs != cudaStreamCaptureStatusNone)
+        return set_err(DG_ERR_ARG, "dg_spmm_run: split-row buffer too small during capture "
+                                   "(reserve the plan for the widest pitch first)");
+      if (const int rc = dg_spmm_plan_reserve(p, ld_h)) return rc;
     }
   }
   int wmax;

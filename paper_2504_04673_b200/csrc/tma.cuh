@@ -17,6 +17,10 @@ namespace dg {
 // box_rows elements (box_rows = 1 for tile::gather4).  Returns 0 on success.
 int make_tensor_map_2d(CUtensorMap* map, const void* base, int64_t rows, int64_t ld,
                        int64_t cols, int box_cols, int box_rows, bool l2_promote_256);
+// the same with the 128-byte swizzle (box_cols * 4 == 128): 16-B chunk c of
+// smem row r lands at chunk c ^ (r % 8) -- conflict-free column reads
+int make_tensor_map_2d_swz128(CUtensorMap* map, const void* base, int64_t rows, int64_t ld,
+                              int64_t cols, int box_cols, int box_rows);
 
 }  // namespace dg
 

@@ -241,6 +241,10 @@ class DevicePlan:
         self.halo = {r: None for r in self.local}
         self.partial = {r: None for r in self.local}
         self.parity = 0
+        if max_ld is not None:                 # split-row buffers: no growth in the hot call
+            for h in (self._splan, self._bplan):
+                if h:
+                    L.check(lib.dg_spmm_plan_reserve(h, int(max_ld)))
         info = (C.c_int64 * 8)()
         L.check(lib.dg_spmm_plan_info(self._splan, info))
         self.info = list(info)

@@ -16,8 +16,14 @@ oracle in float64.
   products graph.
 
 Gradients are read back through the SGD step with a large learning rate:
-W1 = W0 - lr Y, so Y = (W0 - W1) / lr with an fp32 rounding error of
-ulp(lr |Y|) / lr, relative 6e-8.
+W1 = W0 - lr Y, so Y = (W0 - W1) / lr, up to the fp32 rounding of that step,
+1.2e-7 (|W0| + lr |Y|) / lr, which the bound adds.
+
+A ReLU mask is a discontinuity: where a pre-activation is within rounding of
+0 (products-shaped: 3-4 of 39M entries, |z| < 5e-8) the fp32 and float64
+masks may differ.  scripts/diag_grad.py measured its effect at 5.9e-6 of
+Ymag (with the GPU's own masks the float64 chain agrees to 5e-8), inside
+the 1e-5 contract.
 
 Tolerance (written here): loss rtol 1e-5; Y elementwise
 |Y_gpu - Y_ref| <= 1e-5 * Ymag + 1e-30, Ymag = |H|^T (|A^T| |G|) -- the sum
@@ -139,7 +145,9 @@ def _full_epoch_check(a, x, y, wl, p, c, variant, partition=None, lr=100.0):
     assert abs(res.losses[0] - loss_ref) <= 1e-5 * abs(loss_ref), (res.losses[0], loss_ref)
     for l, (w1, yr, mg) in enumerate(zip(res.weights, ys, mags)):
         yg = (w_init[l] - w1.astype(np.float64)) / lr
-        bound = 1e-5 * mg + 6e-8 * np.abs(yr).max() + 1e-30
+        # + the fp32 rounding of the SGD step W1 = fl(W0 - fl(lr Y)) that the
+        # read-back divides by lr
+        bound = 1e-5 * mg + 1.2e-7 * (np.abs(w_init[l]) + lr * np.abs(yr)) / lr + 1e-30
         bad = np.abs(yg - yr) > bound
         assert not bad.any(), (l, float(np.max(np.abs(yg - yr) / (mg + 1e-30))))
         print(f"[{variant} p={p} c={c}] Y_{l}: max |err| / max |Y| = "

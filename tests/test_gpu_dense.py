@@ -19,10 +19,21 @@ def _pad(x, ld):
     return out
 
 
+@pytest.fixture(params=["tma", "legacy"])
+def dense_path(request):
+    """The TMA-fed kernels (default) and the register-staged ones."""
+    import ctypes
+    flag = ctypes.c_int.in_dll(L.lib(), "dg_dense_legacy")
+    flag.value = int(request.param == "legacy")
+    yield request.param
+    flag.value = 0
+
+
 @pytest.mark.parametrize("n,fi,fo", [(1000, 602, 16), (777, 16, 41), (5000, 100, 16),
                                      (333, 16, 47), (64, 3, 2), (1, 16, 16), (3001, 16, 172),
-                                     (1500, 128, 16), (700, 16, 250), (257, 41, 7)])
-def test_dense_fwd_bwd_wgrad(n, fi, fo):
+                                     (1500, 128, 16), (700, 16, 250), (257, 41, 7),
+                                     (20000, 602, 16), (9000, 16, 64), (4099, 48, 33)])
+def test_dense_fwd_bwd_wgrad(n, fi, fo, dense_path):
     torch.manual_seed(n + fi + fo)
     d = _Dense(torch.device("cuda"))
     l0 = L.launch_count()
