@@ -861,7 +861,7 @@ def run_ours(args, wl):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": bench_config(args, wl),
         "run_config": {"reduce_after_transform": bool(args.reduce_after_transform),
-                       "partition": part_name,
+                       "partition": part_name, "rank_map": args.rank_map,
                        "l2": "inputs larger than L2 (H0 = %d MB)" % (gr.x.numel() * 4 // 2**20),
                        "ranks_per_gpu": args.ranks_per_gpu},
         "spmm_hbm_gbs": round(spmm_bytes_epoch / (ms_epoch / 1e3) / 1e9, 1),
@@ -921,10 +921,14 @@ def main():
                     help="auto: block (Reddit) / lpa (products); lpa: label-propagation "
                          "communities packed onto the parts; gvb: the reference's "
                          "greedy-tv -> GVB")
+    ap.add_argument("--rank-map", default="block", choices=["block", "cyclic"],
+                    help="virtual rank -> GPU placement (dist.World.rank_map): block keeps "
+                         "1.5D replicas on one GPU, cyclic spreads them (NVLink reduction)")
     ap.add_argument("--row-order", default="auto", choices=["auto", "none", "lpa"],
                     help="SpMM processing order of each rank's rows (no effect on results); "
                          "auto: lpa for products under a block / gvb partition")
     args = ap.parse_args()
+    os.environ["DG_RANK_MAP"] = args.rank_map
     wl = WORKLOADS[args.workload]
     if args.ranks_per_gpu is None:
         args.ranks_per_gpu = max(1, 4 // args.gpus) if args.workload == "rmat14" else 1

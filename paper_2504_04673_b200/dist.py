@@ -125,8 +125,23 @@ class World:
         if self.multi and int(self._err.item()) != 0:
             raise RuntimeError("device barrier timed out: a peer process stalled")
 
+    @property
+    def rank_map(self):
+        """How virtual ranks map onto processes (DG_RANK_MAP): "block"
+        (default; rank r on process floor(r N / p), so the c replicas of a
+        row group share a GPU when p/N >= c and the row-group reduction runs
+        in HBM) or "cyclic" (rank r on process r mod N: replicas on
+        different GPUs, the reduction crosses NVLink as a reduce-scatter +
+        all-gather; column-group peers share GPUs instead)."""
+        m = os.environ.get("DG_RANK_MAP", "block")
+        if m not in ("block", "cyclic"):
+            raise ValueError(f"DG_RANK_MAP must be 'block' or 'cyclic', got {m!r}")
+        return m
+
     def proc_of(self, rank, p):
-        """Block map of p virtual ranks onto the processes."""
+        """The process hosting virtual rank `rank` of p (see rank_map)."""
+        if self.rank_map == "cyclic":
+            return rank % self.size
         return (rank * self.size) // p
 
     def local_ranks(self, p):

@@ -407,14 +407,50 @@ class DevicePlan:
                     for r in self.local}
         if self.reduce:
             self.world.barrier()                        # every replica's partial is ready
+            spread = [r for r in self.local if self._group_spans_processes(r)]
             for r in self.local:
+                if r in spread:
+                    continue
                 i, _ = self.grid.coords(r)
                 grp = self.grid.row_group(i)
                 n = vp.ranks[r].n_rows * ld
                 L.check(lib.dg_group_reduce(len(grp), L.ptr_array(
                     [self._partial_ptr(m, par) for m in grp]), 1, L.ptr_array([out[r]]), 0,
                     n, 0, st))
+            if spread:
+                self._reduce_scatter_all_gather(spread, par, ld, out, st)
         return out
+
+    def _group_spans_processes(self, r):
+        grp = self.grid.row_group(self.grid.coords(r)[0])
+        return len({self.world.proc_of(m, self.grid.p) for m in grp}) > 1
+
+    def _reduce_scatter_all_gather(self, ranks, par, ld, out, st):
+        """Row-group sum across processes, bandwidth-optimal (reference
+        spmm.py:227, runtime.py:437-466): member k of a c-member group sums
+        chunk k of the n x ld partials -- reading (c-1)/c of the data from
+        its peers -- and stores the sum into chunk k of EVERY member's
+        partial buffer (peer stores); after one device barrier each member
+        copies the whole sum out of its own buffer.  2 (c-1)/c n bytes cross
+        NVLink per member instead of (c-1) n for read-all-partials; every
+        element is reduced once, in ascending member order, so the replicas
+        stay bitwise identical."""
+        lib = L.lib()
+        vp = self.vplan
+        for r in ranks:
+            i, _ = self.grid.coords(r)
+            grp = self.grid.row_group(i)
+            c = len(grp)
+            k = grp.index(r)
+            n = vp.ranks[r].n_rows * ld
+            lo, hi = (n * k // c) // 4 * 4, (n * (k + 1) // c) // 4 * 4 if k + 1 < c else n
+            ptrs = L.ptr_array([self._partial_ptr(m, par) for m in grp])
+            L.check(lib.dg_group_reduce(c, ptrs, c, ptrs, lo, hi, 1, st))
+        self.world.barrier()                            # every chunk landed everywhere
+        for r in ranks:
+            n = vp.ranks[r].n_rows * ld
+            L.check(lib.dg_group_reduce(1, L.ptr_array([self._partial_ptr(r, par)]), 1,
+                                        L.ptr_array([out[r]]), 0, n, 0, st))
 
     # ---- pieces of a phase, for per-kernel timing in bench.py ------------
     def exchange_only(self, hs: dict, f: int, ld: int):

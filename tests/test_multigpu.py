@@ -20,17 +20,22 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("nproc", [2, 4])
-def test_multiprocess_matches_reference(nproc):
+@pytest.mark.parametrize("nproc,rank_map", [(2, "block"), (4, "block"), (2, "cyclic"),
+                                            (4, "cyclic")])
+def test_multiprocess_matches_reference(nproc, rank_map):
+    """block: replicas of a row group share a process; cyclic: they sit on
+    different processes, so 1.5D runs the cross-process reduce-scatter +
+    all-gather (engine.DevicePlan._reduce_scatter_all_gather)."""
     import torch
     ngpu = torch.cuda.device_count()
-    env = dict(os.environ, OMP_NUM_THREADS="2")
+    env = dict(os.environ, OMP_NUM_THREADS="2", DG_RANK_MAP=rank_map)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1",
-           "--master-port", str(29617 + nproc),
+           "--master-port", str(29617 + nproc + (10 if rank_map == "cyclic" else 0)),
            os.path.join(ROOT, "tests", "mp_gpu_worker.py")]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, env=env)
     out = r.stdout[-6000:] + r.stderr[-6000:]
-    print(f"[{nproc} processes on {min(ngpu, nproc)} GPU(s)]\n" + r.stdout[-3000:])
+    print(f"[{nproc} processes on {min(ngpu, nproc)} GPU(s), {rank_map} rank map]\n"
+          + r.stdout[-3000:])
     assert r.returncode == 0, out
     assert out.count("0 failures") == nproc, out

@@ -13,10 +13,10 @@ import torch.multiprocessing as mp
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _worker(rank, world, port, key, q):
+def _worker(rank, world, port, key, q, rank_map="block"):
     sys.path.insert(0, ROOT)
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
-                      WORLD_SIZE=str(world))
+                      WORLD_SIZE=str(world), DG_RANK_MAP=rank_map)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_2504_04673_b200 as P
     from paper_2504_04673_b200.dist import World
@@ -62,12 +62,14 @@ def _worker(rank, world, port, key, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("key", ["c7", "c8", "c12", "c14", "c16"])
-def test_two_process_plan_and_ledger(key):
+@pytest.mark.parametrize("key,rank_map", [("c7", "block"), ("c8", "block"), ("c12", "block"),
+                                          ("c14", "block"), ("c16", "block"), ("c12", "cyclic"),
+                                          ("c16", "cyclic")])
+def test_two_process_plan_and_ledger(key, rank_map):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29500 + int(key[1:]) * 7 + os.getpid() % 1000
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, key, q)) for r in range(2)]
+    port = 29500 + int(key[1:]) * 7 + os.getpid() % 1000 + (3 if rank_map == "cyclic" else 0)
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, key, q, rank_map)) for r in range(2)]
     for pr in procs:
         pr.start()
     res = [q.get(timeout=120) for _ in procs]
@@ -76,3 +78,6 @@ def test_two_process_plan_and_ledger(key):
     assert all(ok for _, ok, _ in res), res
     hosted = sorted(r for _, _, loc in res for r in loc)
     assert hosted == sorted(set(hosted))       # disjoint cover of the ranks
+    if rank_map == "cyclic":
+        for rank, _, loc in res:
+            assert all(r % 2 == rank for r in loc)
