@@ -74,7 +74,7 @@ int dg_spmm_plan_create(dg_spmm_plan** plan, int n_ranks,
  * processed within one window of their row, else one global window).  The order and the
  * window change no result: every row is still summed in its CSR storage order
  * (bit-identical output).  dg_spmm_plan_info reports the window in info[6]. */
-#define DG_SPMM_WINDOW_NNZ (1LL << 22)
+#define DG_SPMM_WINDOW_NNZ (1LL << 20)
 int dg_spmm_plan_create_ordered(dg_spmm_plan** plan, int n_ranks,
                                 const int64_t* n_rows, const int64_t* n_local, const int64_t* nnz,
                                 const int64_t* const* row_ptr, const int32_t* const* col_ext,
