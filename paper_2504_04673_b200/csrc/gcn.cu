@@ -216,8 +216,14 @@ __global__ void __launch_bounds__(256, (K <= 2 ? 3 : 1)) xent_vec_kernel(
       am = grp_min<G>(am);
       const bool on = valid[u] && mask[row] != 0;
       // (softmax - onehot) / denom with one division per row: p_j/denom =
-      // e_j * (1 / (s * denom)); the label term subtracts 1/denom
-      const double scale = 1.0 / (s * denom);
+      // e_j * (1 / (s * denom)); the label term subtracts 1/denom.  The
+      // fp64 division (and the loss's fp64 log below) run on the group's
+      // first lane only and the scale is broadcast: 16-lane groups (C=47)
+      // otherwise spend most of the kernel in redundant fp64 math
+      double scale_l = 0.0;
+      if (lig == 0) scale_l = 1.0 / (s * denom);
+      const double scale =
+          __shfl_sync(0xffffffffu, scale_l, (threadIdx.x & 31) & ~(G - 1));
       const float scale_f = (float)scale;
       const double inv_d = 1.0 / denom;
       float4* gr = reinterpret_cast<float4*>(grad + row * ldg);
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__(256, (K <= 2 ? 3 : 1)) xent_vec_kernel(
       }
       if (valid[u])
         for (int c = lig + K * G; c < gchunk; c += G) gr[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (on) {
+      if (on && lig == 0) {
         loss += log(s) - xl;
         corr += (am == lbl) ? 1.0 : 0.0;
       }
