@@ -845,6 +845,9 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   // 128-bit lanes for rows of up to 48 floats: f=41/47 rows take 12 lane-
   // chunks of 16 B (3 per lane) instead of 6 x 32 B with two idle lanes of
   // eight, 1.66 vs 1.77 ms (profiles/r01/spmm_f41_lanes.txt)
+  // (round 2, products-shaped with LPA order: 256-bit lanes for 17..48
+  // floats 2.99 vs 2.72 ms at f=47; for all 9..48 floats f=16 1.42 vs 1.22 ms;
+  // one 128-bit chunk per lane (G=16) at f=47 3.80 ms -- profiles/r02/r2_lanes_*)
   bool v8 = (f > 48 || (f > 8 && f <= 16 && acc == 2 && dram_table)) && ld_h % 8 == 0 &&
             ld_z % 8 == 0;
   for (int r = 0; r < p->n_ranks && v8; ++r) {
@@ -899,6 +902,7 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
   }
   int G, CPL, ns;
   choose_config(chunks, wmax, &G, &CPL, &ns);
+
   const bool two = acc == 2 && v8;
   if (two) {
     // one chunk per lane (the two-level kernel's shape): the narrowest

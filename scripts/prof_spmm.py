@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--order", default="none", choices=["none", "lpa", "lpa-part"],
                     help="lpa: SpMM row order by label-propagation communities (plan only); "
                          "lpa-part: relabel the graph by lpa_partition(k=1) (as bench.py)")
+    ap.add_argument("--slab-major", type=int, default=0,
+                    help="also time the wide layer from a slab-major copy of H: slabs of this "
+                         "many floats stored contiguously, one dg_spmm_run per slab")
     ap.add_argument("--window", type=int, default=0,
                     help="entries per length-bucketing window of the plan (0: default)")
     ap.add_argument("--cusparse", action="store_true",
@@ -78,6 +81,34 @@ def main():
                 print(f"f={f} slab={slab} acc={acc} chunk={args.chunk}: {t:.3f} ms  "
                       f"gather {gather / t / 1e6:.0f} GB/s  nnz*f/s {a.nnz * f / t / 1e6:.3g} G",
                       flush=True)
+        if args.slab_major and f > args.slab_major:
+            sw = args.slab_major
+            ns = (f + sw - 1) // sw
+            slabs = [h[:, k * sw:min(f, (k + 1) * sw)].contiguous() for k in range(ns)]
+            slabs = [torch.nn.functional.pad(x, (0, (-x.shape[1]) % 8)) for x in slabs]
+            z2 = torch.zeros_like(z)
+
+            def go_sm():
+                for k, x in enumerate(slabs):
+                    fk = min(f, (k + 1) * sw) - k * sw
+                    L.check(lib.dg_spmm_run(dp._splan, L.ptr_array([x]), L.ptr_array([x]),
+                                            L.ptr_array([z2[:, k * sw:].data_ptr()]), fk,
+                                            x.shape[1], ld, 2, 0, 0, L.stream_ptr()))
+            go_sm()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.reps):
+                go_sm()
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / args.reps
+            full = (f // sw) * sw          # a narrow last slab takes the <= 48-float kernel
+            same = bool(torch.equal(z2[:, :full], z[:, :full]))
+            print(f"f={f} slab-major {sw}-float slabs ({ns} launches): {t:.3f} ms  "
+                  f"gather {4.0 * f * a.nnz / t / 1e6:.0f} GB/s  bitwise equal to row-major: {same}",
+                  flush=True)
         if args.cusparse:
             import numpy as np
             sp = torch.sparse_csr_tensor(torch.from_numpy(a.row_ptr), torch.from_numpy(a.col_idx),
