@@ -142,13 +142,66 @@ def make_inputs(wl, n, seed=1):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed
+    region: NVML queried from a background thread every 2 ms (so even a
+    12 ms timed region of config 1 gets samples), one sample at start and at
+    stop; nvidia-smi polling (100 ms) when NVML is unavailable."""
 
-    def __init__(self, gpu=0):
+    _REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                "sw_power_cap": 0x4}
+
+    def __init__(self, gpu=0, period_s=0.002):
+        import threading
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.p = None
+        self._stop = threading.Event()
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = self._handle(N, gpu)
+            self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM))
+            self._sample()
+            self.t = threading.Thread(target=self._loop, args=(period_s,), daemon=True)
+            self.t.start()
+            self.source = "nvml (2 ms)"
+        except Exception:  # noqa: BLE001 - fall back to nvidia-smi polling
+            self.N = None
+            self._start_smi(gpu)
+
+    @staticmethod
+    def _handle(N, gpu):
+        try:
+            import torch
+            uuid = str(torch.cuda.get_device_properties(gpu).uuid)
+            return N.nvmlDeviceGetHandleByUUID(("GPU-" + uuid).encode())
+        except Exception:  # noqa: BLE001
+            return N.nvmlDeviceGetHandleByIndex(gpu)
+
+    def _sample(self):
+        N = self.N
+        self.samples.append(float(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)))
+        try:
+            mask = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except AttributeError:
+            mask = N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        for name, bit in self._REASONS.items():
+            if mask & bit:
+                self.reasons.add(name)
+
+    def _loop(self, period):
+        while not self._stop.wait(period):
+            try:
+                self._sample()
+            except Exception:  # noqa: BLE001
+                return
+
+    def _start_smi(self, gpu):
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
+        self.source = "nvidia-smi (100 ms)"
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(gpu), f"--query-gpu={q}",
                                        "--format=csv,noheader,nounits", "-lms", "100"],
@@ -157,6 +210,14 @@ class ClockSampler:
             self.p = None
 
     def stop(self):
+        if self.N is not None:
+            self._stop.set()
+            self.t.join()
+            self._sample()
+            sm = self.samples
+            return {"sm_mhz": statistics.median(sm), "sm_max_mhz": self.max_mhz,
+                    "reasons": sorted(self.reasons), "samples": len(sm),
+                    "sm_mhz_min": min(sm), "source": self.source}
         if self.p is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
@@ -180,7 +241,7 @@ class ClockSampler:
         os.unlink(self.f.name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "source": self.source}
 
 
 # ---------------------------------------------------------------------------

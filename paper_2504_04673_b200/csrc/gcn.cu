@@ -137,7 +137,7 @@ __device__ __forceinline__ int grp_min(int v) {
 // order in the last CTA).
 // 3 CTAs/SM for rows <= 256 classes (C=172: 20.9 -> 17.5 ms at 27.8M rows).
 template <int G, int K>
-__global__ void __launch_bounds__(256, (K <= 2 ? 3 : 1)) xent_vec_kernel(
+__global__ void __launch_bounds__(256, (K <= 2 ? 3 : 2)) xent_vec_kernel(
     const float* __restrict__ x, int64_t n, int C, int64_t ld, const int64_t* __restrict__ labels,
     const uint8_t* __restrict__ mask, double denom, float* __restrict__ grad, int64_t ldg,
     double* scratch, unsigned* counter, double* out) {
@@ -327,8 +327,12 @@ int dg_xent(const float* logits, int64_t n, int32_t C, int64_t ld, const int64_t
   if (n < 1 || C < 1 || C > ld || C > ld_grad) return set_err(DG_ERR_ARG, "xent: bad args");
   const bool vec = ld % 4 == 0 && ld_grad % 4 == 0 && (((uintptr_t)logits | (uintptr_t)grad) & 15) == 0;
   const int nchunk = (C + 3) / 4;
+  // lanes per row: the narrowest power of two that keeps <= 4 float4 chunks
+  // per lane -- fewer lanes per row means fewer shuffle steps and fewer
+  // redundant per-row instructions (C=47: 16 lanes x 1 chunk was issue-bound
+  // at 447M warp instructions, ncu profiles/r02; 4 lanes x 3 chunks)
   int G = 1;
-  while (G < nchunk && G < 32) G <<= 1;
+  while (G * 4 < nchunk && G < 32) G <<= 1;
   const int K = (nchunk + G - 1) / G;
   if (vec && K <= 4) {
     const int rpb = (256 / G) * 4;                   // rows per CTA step (RU = 4)
@@ -337,17 +341,22 @@ int dg_xent(const float* logits, int64_t n, int32_t C, int64_t ld, const int64_t
 #define DG_XV(g, k) xent_vec_kernel<g, k><<<blocks, 256, 0, st>>>(logits, n, C, ld, labels, mask, \
                                                                   denom, grad, ld_grad, scratch, \
                                                                   counter, stats_out)
+#define DG_XVK(g)                 \
+  switch (K) {                    \
+    case 1: DG_XV(g, 1); break;   \
+    case 2: DG_XV(g, 2); break;   \
+    case 3: DG_XV(g, 3); break;   \
+    default: DG_XV(g, 4); break;  \
+  }
     switch (G) {
-      case 1: DG_XV(1, 1); break;
-      case 2: DG_XV(2, 1); break;
-      case 4: DG_XV(4, 1); break;
-      case 8: DG_XV(8, 1); break;
-      case 16: DG_XV(16, 1); break;
-      default:
-        if (K == 1) DG_XV(32, 1);
-        else if (K == 2) DG_XV(32, 2);
-        else DG_XV(32, 4);
+      case 1: DG_XVK(1); break;
+      case 2: DG_XVK(2); break;
+      case 4: DG_XVK(4); break;
+      case 8: DG_XVK(8); break;
+      case 16: DG_XVK(16); break;
+      default: DG_XVK(32); break;
     }
+#undef DG_XVK
 #undef DG_XV
   } else {
     const unsigned blocks = (unsigned)std::min<int64_t>((n + 7) / 8, 4 * 148);

@@ -17,7 +17,7 @@
 //    request.  Wide layers are split into slabs (grid.y) sized so one slab of
 //    all gathered rows stays L2-resident; the CSR stream is evict-first.
 //  * Two forms.  128-bit lanes (rows <= 48 floats): entries loaded with
-//    uniform 16-B vector loads one step ahead, 4-entry fp32 windows folded
+//    uniform 16-B vector loads one step ahead, 8-entry fp32 windows folded
 //    into fp64 accumulators.  acc = 2 with 256-bit lanes (rows > 48 floats,
 //    and 9..16-float rows of tables far larger than L2): one chunk per lane, the item's
 //    entries staged in shared memory by cp.async one window ahead (no
@@ -85,8 +85,6 @@ __device__ __forceinline__ int4 ld_stream(const int4* p, uint64_t pol) {
       : "l"(p), "l"(pol));
   return v;
 }
-
-__device__ __forceinline__ float4 ld_h(const float4* p) { return __ldg(p); }
 
 // Occupancy vs in-flight loads (measured on B200, Reddit-shaped graph):
 // one float4 chunk per lane -> 4 entries per step and >= 4 CTAs/SM (<= 64
@@ -166,6 +164,13 @@ __global__ void __launch_bounds__(256, MB)
   const float* __restrict__ hl = R.hl;
   const float* __restrict__ hh = R.hh;
   const int64_t nl = R.n_local;
+  // one base-pointer select per gather (own block, or the halo buffer
+  // pre-offset by -n_local rows) and a 32 x 32 -> 64-bit row offset: f=602
+  // 18.3 -> 17.6 ms, f=41 1.70 -> 1.54 ms, products f=100 5.15 -> 4.84 ms
+  // (profiles/r02/r2_v2_*)
+  const int nl32 = (int)nl;
+  const int ld32 = (int)ld;
+  const float* hh_off = hh - nl * ld;       // halo row c lives at hh_off + c * ld
   const uint64_t pol = evict_first_policy();
 
   int chk[CPL];                             // chunk index (units of V floats)
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(256, MB)
         const int c = (j & 1) ? cur[j >> 1].z : cur[j >> 1].x;
         v[j] = __int_as_float((j & 1) ? cur[j >> 1].w : cur[j >> 1].y);
         if (j < nv) {
-          const float* hp = c < nl ? hl + (int64_t)c * ld : hh + (int64_t)(c - nl) * ld;
+          const float* hp = (c < nl32 ? hl : hh_off) + (int64_t)c * ld32;
   #pragma unroll
           for (int q = 0; q < CPL; ++q) {
             if (on[q]) x[j][q].load(hp + (int64_t)chk[q] * V);
@@ -241,13 +246,15 @@ __global__ void __launch_bounds__(256, MB)
   #pragma unroll
           for (int k = 0; k < V; ++k) part[q][k] = fmaf(v[j], x[j][q].v[k], part[q][k]);
       if constexpr (F64) {
+        if ((s & 1) || s + 1 == steps) {      // 8-entry fp32 windows into fp64
   #pragma unroll
-        for (int q = 0; q < CPL; ++q)
+          for (int q = 0; q < CPL; ++q)
   #pragma unroll
-          for (int k = 0; k < V; ++k) {
-            acc[q][k] += (double)part[q][k];
-            part[q][k] = 0.f;
-          }
+            for (int k = 0; k < V; ++k) {
+              acc[q][k] += (double)part[q][k];
+              part[q][k] = 0.f;
+            }
+        }
       } else if constexpr (TWO) {
         constexpr int WS = 32 / E;            // steps per 32-entry window
         if (s % WS == WS - 1) {
@@ -300,7 +307,7 @@ __global__ void __launch_bounds__(256, MB)
           v[j] = __int_as_float(en.y);
           if (j < nv) {
             const int c = en.x;
-            const float* hp = c < nl ? hl + (int64_t)c * ld : hh + (int64_t)(c - nl) * ld;
+            const float* hp = (c < nl32 ? hl : hh_off) + (int64_t)c * ld32;
 #pragma unroll
             for (int q = 0; q < CPL; ++q) {
               if (on[q]) x[j][q].load(hp + (int64_t)chk[q] * V);
