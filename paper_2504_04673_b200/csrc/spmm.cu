@@ -477,7 +477,10 @@ LaunchFn pick_two(int G) {
     case 2: return &launch_spmm<2, 1, false, 8, 4, 2, true, true>;
     case 4: return &launch_spmm<4, 1, false, 8, 4, 2, true, true>;
     case 8: return &launch_spmm<8, 1, false, 8, 4, 2, true, true>;
-    case 16: return &launch_spmm<16, 1, false, 8, 4, 2, true, true>;
+    // 16-lane groups (97..128-float rows: products f=100, papers f=128; the
+    // gathers miss L2 often): 4 entries per step at 3 CTAs/SM keep more bytes
+    // in flight than 2 at 4 CTAs/SM -- products f=100 4.84 -> 4.76 ms
+    case 16: return &launch_spmm<16, 1, false, 8, 3, 4, true, true>;
     case 32: return &launch_spmm<32, 1, false, 8, 4, 2, true, true>;
     default: return nullptr;
   }
