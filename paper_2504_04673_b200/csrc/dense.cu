@@ -151,9 +151,12 @@ __global__ void __launch_bounds__(288, 2) dense_rows_tma_kernel(
     float* __restrict__ Crelu, const float* __restrict__ Zmask, int64_t ldm) {
   constexpr int TN = NP / 4;                         // columns per thread
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-B alignment of the ring (128-byte swizzle atoms)
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B alignment of the ring (128-byte swizzle atoms), computed in the
+  // shared window and applied as an offset to the shared array -- an integer
+  // round trip of the pointer would turn every ring / B read into a generic
+  // load (ncu: LG-throttle and L1TEX stalls, 0.22 ms at K=602)
+  const uint32_t s0 = smem_u32(smem_raw);
+  unsigned char* base = smem_raw + (((s0 + 1023u) & ~1023u) - s0);
   unsigned char* ring = base;
   uint64_t* full = reinterpret_cast<uint64_t*>(base + TR_STAGES * TR_STAGE_BYTES);
   uint64_t* empty = full + TR_STAGES;
