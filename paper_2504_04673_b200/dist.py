@@ -62,16 +62,20 @@ class World:
         the device barrier flags.  Idempotent."""
         if self.device is not None:
             return self
+        if not torch.cuda.is_available():
+            # host-only use (the generic Comm primitives over gloo, CPU tests):
+            # no device buffers, host barriers
+            self.device = torch.device("cpu")
+            self.barrier_mode = "host"
+            if self.multi:
+                self._init_pg()
+            return self
         if self.multi:
             torch.cuda.set_device(self.local % max(torch.cuda.device_count(), 1))
         self.device = torch.device("cuda", torch.cuda.current_device())
         if not self.multi:
             return self
-        import torch.distributed as dist
-        if not dist.is_initialized():
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            dist.init_process_group("gloo", rank=self.proc, world_size=self.size)
-        self._pg = dist.group.WORLD
+        self._init_pg()
         lib = L.lib()
         for d in range(torch.cuda.device_count()):
             if d != torch.cuda.current_device():
@@ -91,6 +95,13 @@ class World:
                              "kernels in different contexts are not co-scheduled")
         self.barrier_mode = mode
         return self
+
+    def _init_pg(self):
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo", rank=self.proc, world_size=self.size)
+        self._pg = dist.group.WORLD
 
     def all_gather_object(self, obj):
         if not self.multi:
@@ -112,7 +123,8 @@ class World:
         if not self.multi:
             return
         if self.barrier_mode == "host":
-            torch.cuda.current_stream().synchronize()
+            if self.device.type == "cuda":
+                torch.cuda.current_stream().synchronize()
             self.host_barrier()
             return
         self._epoch += 1
@@ -122,7 +134,7 @@ class World:
 
     def check(self):
         """Raise if a device barrier timed out (call at sync points)."""
-        if self.multi and int(self._err.item()) != 0:
+        if self.multi and self._err is not None and int(self._err.item()) != 0:
             raise RuntimeError("device barrier timed out: a peer process stalled")
 
     @property

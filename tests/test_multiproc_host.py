@@ -81,3 +81,63 @@ def test_two_process_plan_and_ledger(key, rank_map):
     if rank_map == "cyclic":
         for rank, _, loc in res:
             assert all(r % 2 == rank for r in loc)
+
+
+def _generic_worker(rank, world, port, q):
+    """Rank programs using the reference's generic Comm primitives across
+    processes (gloo): a ring of isend/recv, all_to_allv and broadcast."""
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import paper_2504_04673_b200 as P
+    p = 4
+
+    def program(comm):
+        r = comm.rank
+        comm.isend((r + 1) % p, np.arange(3, dtype=np.float64) + 10 * r, tag=5)
+        comm.isend((r + 2) % p, np.full((2, 2), r, dtype=np.int64), tag="idx")
+        got = comm.recv((r - 1) % p, tag=5)
+        got2 = comm.recv((r - 2) % p, tag="idx")
+        a2a = comm.all_to_allv([np.full(d + 1, 100 * r + d, dtype=np.float64) for d in range(p)])
+        b = comm.broadcast(2, np.arange(5, dtype=np.float64) * 7 if r == 2 else None)
+        return {"ring": got, "ring2": got2, "a2a": a2a, "b": b}
+
+    run = P.run_program(p, 1, program)
+    q.put((rank, run.results, run.ledger.to_dict()))
+
+
+def test_generic_primitives_across_processes():
+    """isend / recv / all_to_allv / broadcast between ranks of different
+    processes give the reference's results and ledger (same as one process)."""
+    import paper_2504_04673_b200 as P
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29400 + os.getpid() % 1000
+    procs = [ctx.Process(target=_generic_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for pr in procs:
+        pr.join(timeout=60)
+    p = 4
+
+    def program(comm):
+        r = comm.rank
+        comm.isend((r + 1) % p, np.arange(3, dtype=np.float64) + 10 * r, tag=5)
+        comm.isend((r + 2) % p, np.full((2, 2), r, dtype=np.int64), tag="idx")
+        got = comm.recv((r - 1) % p, tag=5)
+        got2 = comm.recv((r - 2) % p, tag="idx")
+        a2a = comm.all_to_allv([np.full(d + 1, 100 * r + d, dtype=np.float64) for d in range(p)])
+        b = comm.broadcast(2, np.arange(5, dtype=np.float64) * 7 if r == 2 else None)
+        return {"ring": got, "ring2": got2, "a2a": a2a, "b": b}
+
+    os.environ.pop("WORLD_SIZE", None)
+    ref = P.run_program(p, 1, program)
+    for _, results, led in res:
+        assert led == ref.ledger.to_dict()
+        for r in range(p):
+            assert np.array_equal(results[r]["ring"], ref.results[r]["ring"])
+            assert np.array_equal(results[r]["ring2"], ref.results[r]["ring2"])
+            assert np.array_equal(results[r]["b"], ref.results[r]["b"])
+            for x, y in zip(results[r]["a2a"], ref.results[r]["a2a"]):
+                assert np.array_equal(x, y)
