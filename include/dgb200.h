@@ -84,6 +84,16 @@ int dg_spmm_plan_destroy(dg_spmm_plan* plan);
 /* Size the plan's fp64 split-row partial buffer for row pitches up to ld_max, so that
  * dg_spmm_run never allocates (it refuses to grow the buffer inside a stream capture). */
 int dg_spmm_plan_reserve(dg_spmm_plan* plan, int64_t ld_max);
+/* Fused forward epilogue (gcn.py:273-276): z[r] = (A_r [H_r; halo_r]) W and,
+ * when h_relu is given, h_relu[r] = relu(z[r]) -- the product T never reaches HBM.  For
+ * 13 <= f <= 16 (one float4 per lane of a 4-lane group), W is f x n_out (row pitch ld_w,
+ * device), n_out <= 64, z / h_relu rows of pitch ld_z (>= n_out, padding written as 0).
+ * Single-pass plans only (no split own/halo passes, no 1.5D partials).  T is summed
+ * exactly as dg_spmm_run sums it; z = t W in fp32 in ascending k. */
+int dg_spmm_run_fused(dg_spmm_plan* plan, const float* const* h_local,
+                      const float* const* h_halo, float* const* z, float* const* h_relu,
+                      int32_t f, int64_t ld_h, int64_t ld_z, const float* w, int64_t ld_w,
+                      int32_t n_out, void* stream);
 /* info[0]=items, [1]=split rows, [2]=chunks, [3]=total nnz, [4]=device bytes,
  * [5]=extended rows, [6]=length-bucketing window (entries) */
 int dg_spmm_plan_info(const dg_spmm_plan* plan, int64_t info[8]);

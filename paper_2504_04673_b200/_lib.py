@@ -51,6 +51,8 @@ _SIGS = {
     "dg_spmm_plan_info": (C.c_int, [c_vp, c_i64p]),
     "dg_spmm_run": (C.c_int, [c_vp, c_vpp, c_vpp, c_vpp, C.c_int32, C.c_int64, C.c_int64,
                               C.c_int32, C.c_int32, C.c_int32, c_vp]),
+    "dg_spmm_run_fused": (C.c_int, [c_vp, c_vpp, c_vpp, c_vpp, c_vpp, C.c_int32, C.c_int64,
+                                    C.c_int64, c_vp, C.c_int64, C.c_int32, c_vp]),
     "dg_xchg_plan_create": (C.c_int, [c_vpp, C.c_int, c_i32p, c_i64p, c_vpp, c_i64p, c_i32p,
                                       c_i64p]),
     "dg_xchg_plan_destroy": (C.c_int, [c_vp]),

@@ -54,6 +54,7 @@ struct RankArgs {
   const float* hl;     // own H block (ext < n_local)
   const float* hh;     // halo rows (ext >= n_local)
   float* z;
+  float* hr;           // fused epilogue: relu(z) (nullable)
   int64_t n_local;
 };
 
@@ -68,6 +69,10 @@ struct SpmmArgs {
   int32_t chunks;      // ceil(f / 4): float4 chunks that carry features
   int32_t slab;        // chunks per slab (= G * CPL)
   int32_t beta;        // 1: z += result (boundary pass of an overlapped phase)
+  // fused forward epilogue (FN > 0): z = (A H) W, hr = relu(z); W is f x n_out
+  const float* w;
+  int32_t ld_w;
+  int32_t n_out;
 };
 
 __device__ __forceinline__ uint64_t evict_first_policy() {
@@ -143,15 +148,29 @@ struct Vec<8> {
 // STG (experiment): the item's entries are staged into shared memory by
 // cp.async one 2G-entry window ahead (no registers held by the CSR
 // prefetch); every lane reads the window's (col, val) pairs as broadcasts.
+// FN > 0: fused forward epilogue for 13..16-float rows (G = 4
+// lanes x one float4, fp64 folds): the row of T = A H never leaves the
+// registers -- the four lanes swap their quarters, each computes FN/4
+// columns of z = t W from W in shared memory and stores z and relu(z).
 template <int G, int CPL, bool F64, int V, int MB = Tune<CPL, V>::MINB,
-          int EE = Tune<CPL, V>::E, bool TWO = false, bool STG = false>
+          int EE = Tune<CPL, V>::E, bool TWO = false, bool STG = false, int FN = 0>
 __global__ void __launch_bounds__(256, MB)
     spmm_kernel(const __grid_constant__ SpmmArgs a) {
   constexpr int E = EE;                     // entries per pipeline step
   static_assert(!(TWO && F64), "TWO is an fp32 mode");
+  static_assert(FN == 0 || (G == 4 && CPL == 1 && V == 4 && F64 && !STG),
+                "fused epilogue: 16-float rows only");
   constexpr int WIN = 2 * G;                // STG: entries per staged window (16 B per lane)
   static_assert(!STG || (WIN % E == 0), "STG: window must hold whole steps");
   __shared__ __align__(16) int2 stg[STG ? 256 / G : 1][2][STG ? WIN : 1];
+  __shared__ __align__(16) float Ws[FN > 0 ? 16 * FN : 1];
+  if constexpr (FN > 0) {                   // W (16 x FN, zero padded), before any exit
+    for (int i = threadIdx.x; i < 16 * FN; i += blockDim.x) {
+      const int k = i / FN, j = i % FN;
+      Ws[i] = (k < 16 && j < a.n_out) ? a.w[(int64_t)k * a.ld_w + j] : 0.f;
+    }
+    __syncthreads();
+  }
   constexpr int E4 = E / 2;                 // int4 loads per step
   const int lig = threadIdx.x & (G - 1);
   const int64_t gid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -359,6 +378,49 @@ __global__ void __launch_bounds__(256, MB)
       for (int k = 0; k < V; ++k) part[q][k] += acc2[q][k];
   }
 
+  if constexpr (FN > 0) {
+    // the group's four lanes hold t[4 lig .. 4 lig + 3]; swap the quarters
+    const int gbase = (threadIdx.x & 31) & ~3;
+    const unsigned gm = 0xFu << gbase;
+    float mine[4], t[16];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) mine[e] = (float)acc[0][e];
+#pragma unroll
+    for (int src = 0; src < 4; ++src)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) t[4 * src + e] = __shfl_sync(gm, mine[e], gbase + src);
+    if (it.slot < 0) {
+      constexpr int NPL = FN / 4;             // output columns per lane
+      float zz[NPL];
+#pragma unroll
+      for (int j = 0; j < NPL; ++j) zz[j] = 0.f;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float4* wr = reinterpret_cast<const float4*>(Ws + k * FN + lig * NPL);
+#pragma unroll
+        for (int j4 = 0; j4 < NPL / 4; ++j4) {
+          const float4 wv = wr[j4];
+          zz[4 * j4 + 0] = fmaf(t[k], wv.x, zz[4 * j4 + 0]);
+          zz[4 * j4 + 1] = fmaf(t[k], wv.y, zz[4 * j4 + 1]);
+          zz[4 * j4 + 2] = fmaf(t[k], wv.z, zz[4 * j4 + 2]);
+          zz[4 * j4 + 3] = fmaf(t[k], wv.w, zz[4 * j4 + 3]);
+        }
+      }
+      float* zp = R.z + (int64_t)it.row * a.ld_z + lig * NPL;
+      float* hp = R.hr ? R.hr + (int64_t)it.row * a.ld_z + lig * NPL : nullptr;
+#pragma unroll
+      for (int j4 = 0; j4 < NPL / 4; ++j4) {
+        if (lig * NPL + 4 * j4 >= a.ld_z) break;
+        *reinterpret_cast<float4*>(zp + 4 * j4) =
+            make_float4(zz[4 * j4], zz[4 * j4 + 1], zz[4 * j4 + 2], zz[4 * j4 + 3]);
+        if (hp)
+          *reinterpret_cast<float4*>(hp + 4 * j4) =
+              make_float4(fmaxf(zz[4 * j4], 0.f), fmaxf(zz[4 * j4 + 1], 0.f),
+                          fmaxf(zz[4 * j4 + 2], 0.f), fmaxf(zz[4 * j4 + 3], 0.f));
+      }
+      return;
+    }
+  }
   if (it.slot < 0) {
     float* zp = R.z + (int64_t)it.row * a.ld_z;
 #pragma unroll
@@ -419,6 +481,7 @@ __global__ void __launch_bounds__(256, MB)
 
 struct FixArgs {
   float* z[DG_MAX_LOCAL];
+  float* hr[DG_MAX_LOCAL];   // fused epilogue: relu(z) (nullable)
   const Fixup* fix;
   const double* part;
   int64_t ld_z;
@@ -435,6 +498,30 @@ __global__ void __launch_bounds__(128) spmm_fixup_kernel(const __grid_constant__
     for (int k = 0; k < fx.n; ++k) s += a.part[(int64_t)(fx.slot0 + k) * a.ld_part + c];
     if (a.beta) s += (double)zp[c];
     zp[c] = (float)s;
+  }
+}
+
+// fused epilogue for the split rows: t = the ordered sum of the row's
+// partials (as spmm_fixup_kernel), then z = t W, relu(z)
+__global__ void __launch_bounds__(128) spmm_fixup_fused_kernel(
+    const __grid_constant__ FixArgs a, const float* __restrict__ w, int ld_w, int n_out) {
+  __shared__ float t[16];
+  const Fixup fx = a.fix[blockIdx.x];
+  if (threadIdx.x < 16) {
+    double s = 0.0;
+    if (threadIdx.x < a.nfloat)
+      for (int k = 0; k < fx.n; ++k) s += a.part[(int64_t)(fx.slot0 + k) * a.ld_part + threadIdx.x];
+    t[threadIdx.x] = (float)s;
+  }
+  __syncthreads();
+  float* zp = a.z[fx.rank] + (int64_t)fx.row * a.ld_z;
+  float* hp = a.hr[fx.rank];
+  for (int j = threadIdx.x; j < a.ld_z; j += blockDim.x) {
+    float v = 0.f;
+    if (j < n_out)
+      for (int k = 0; k < 16; ++k) v = fmaf(t[k], w[(int64_t)k * ld_w + j], v);
+    zp[j] = v;
+    if (hp) hp[(int64_t)fx.row * a.ld_z + j] = fmaxf(v, 0.f);
   }
 }
 
@@ -877,7 +964,7 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
     const uintptr_t al = (uintptr_t)h_local[r] | (uintptr_t)z[r] |
                          (uintptr_t)(h_halo ? h_halo[r] : nullptr);
     if (al & 15) return set_err(DG_ERR_ARG, "dg_spmm_run: H/Z must be 16-byte aligned");
-    a.r[r] = RankArgs{p->ent[r], h_local[r], h_halo ? h_halo[r] : nullptr, z[r],
+    a.r[r] = RankArgs{p->ent[r], h_local[r], h_halo ? h_halo[r] : nullptr, z[r], nullptr,
                       p->n_local[r]};
     ext_total += p->ext_rows[r];
   }
@@ -951,6 +1038,77 @@ int dg_spmm_run(dg_spmm_plan* p, const float* const* h_local, const float* const
     fa.nfloat = std::min<int>(chunks * V, (int)ld_z);
     fa.beta = beta ? 1 : 0;
     spmm_fixup_kernel<<<(unsigned)p->n_fix, 128, 0, S(stream)>>>(fa);
+    DG_LAUNCHED();
+  }
+  return DG_OK;
+}
+
+int dg_spmm_run_fused(dg_spmm_plan* p, const float* const* h_local, const float* const* h_halo,
+                      float* const* z, float* const* h_relu, int32_t f, int64_t ld_h,
+                      int64_t ld_z, const float* w, int64_t ld_w, int32_t n_out, void* stream) {
+  if (!p) return set_err(DG_ERR_ARG, "dg_spmm_run_fused: null plan");
+  if (f < 13 || f > 16 || ld_h < 16 || ld_h % 4 || n_out < 1 || n_out > 64 || ld_z < n_out ||
+      ld_z % 4 || ld_w < n_out || !w)
+    return set_err(DG_ERR_ARG, "dg_spmm_run_fused: needs 13 <= f <= 16, n_out <= 64, "
+                               "ld_z >= n_out, ld % 4 == 0");
+  const int FN = (n_out + 15) / 16 * 16;
+  if (ld_z > FN) return set_err(DG_ERR_ARG, "dg_spmm_run_fused: ld_z beyond the padded width");
+  SpmmArgs a;
+  std::memset(&a, 0, sizeof(a));
+  for (int r = 0; r < p->n_ranks; ++r) {
+    const uintptr_t al = (uintptr_t)h_local[r] | (uintptr_t)z[r] |
+                         (uintptr_t)(h_halo ? h_halo[r] : nullptr) |
+                         (uintptr_t)(h_relu ? h_relu[r] : nullptr);
+    if (al & 15) return set_err(DG_ERR_ARG, "dg_spmm_run_fused: pointers must be 16-B aligned");
+    a.r[r] = RankArgs{p->ent[r], h_local[r], h_halo ? h_halo[r] : nullptr, z[r],
+                      h_relu ? h_relu[r] : nullptr, p->n_local[r]};
+  }
+  if (p->n_slots) {
+    const int64_t need = p->n_slots * ld_h;
+    if (need > p->part_cap) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      DG_CK(cudaStreamIsCapturing(S(stream), &cs));
+      if (cs != cudaStreamCaptureStatusNone)
+        return set_err(DG_ERR_ARG, "dg_spmm_run_fused: split-row buffer too small during capture");
+      if (const int rc = dg_spmm_plan_reserve(p, ld_h)) return rc;
+    }
+  }
+  a.items = p->items;
+  a.part = p->part;
+  a.n_items = p->n_items;
+  a.ld_h = ld_h;
+  a.ld_z = ld_z;
+  a.ld_part = ld_h;
+  a.chunks = 4;
+  a.slab = 4;
+  a.beta = 0;
+  a.w = w;
+  a.ld_w = (int32_t)ld_w;
+  a.n_out = n_out;
+  if (p->n_items) {
+    const unsigned gx = (unsigned)((p->n_items * 4 + 255) / 256);
+    switch (FN) {
+      case 16: spmm_kernel<4, 1, true, 4, 4, 4, false, false, 16><<<gx, 256, 0, S(stream)>>>(a); break;
+      case 32: spmm_kernel<4, 1, true, 4, 4, 4, false, false, 32><<<gx, 256, 0, S(stream)>>>(a); break;
+      case 48: spmm_kernel<4, 1, true, 4, 4, 4, false, false, 48><<<gx, 256, 0, S(stream)>>>(a); break;
+      default: spmm_kernel<4, 1, true, 4, 4, 4, false, false, 64><<<gx, 256, 0, S(stream)>>>(a); break;
+    }
+    DG_LAUNCHED();
+  }
+  if (p->n_fix) {
+    FixArgs fa;
+    std::memset(&fa, 0, sizeof(fa));
+    for (int r = 0; r < p->n_ranks; ++r) {
+      fa.z[r] = z[r];
+      fa.hr[r] = h_relu ? h_relu[r] : nullptr;
+    }
+    fa.fix = p->fix;
+    fa.part = p->part;
+    fa.ld_z = ld_z;
+    fa.ld_part = ld_h;
+    fa.nfloat = f;
+    fa.beta = 0;
+    spmm_fixup_fused_kernel<<<(unsigned)p->n_fix, 128, 0, S(stream)>>>(fa, w, (int)ld_w, n_out);
     DG_LAUNCHED();
   }
   return DG_OK;

@@ -452,6 +452,36 @@ class DevicePlan:
             L.check(lib.dg_group_reduce(1, L.ptr_array([self._partial_ptr(r, par)]), 1,
                                         L.ptr_array([out[r]]), 0, n, 0, st))
 
+    def can_fuse(self, f, n_out):
+        """Whether `run_fused` applies: a single-pass plan (one process, no
+        own/halo split), no 1.5D partials, 13..16-float rows, n_out <= 64."""
+        return (not self.multi) and (not self.reduce) and 13 <= int(f) <= 16 and \
+            int(n_out) <= 64
+
+    def run_fused(self, hs: dict, f: int, ld: int, w, n_out: int, ld_out: int, z: dict,
+                  h: dict = None):
+        """One multiply phase with the forward transform fused into the SpMM
+        epilogue (gcn.py:273-276): z[r] = (A_r [H_r; halo]) W, h[r] = relu(z[r])
+        -- T never reaches HBM.  `w` (f x n_out, padded pitch) is the layer's
+        weight, identical on every rank (replicated, gcn.py:263)."""
+        if not self.can_fuse(f, n_out):
+            raise ValueError("run_fused: needs a single-pass 1D plan and 13 <= f <= 16, "
+                             "n_out <= 64")
+        lib = L.lib()
+        st = _stream()
+        vp = self.vplan
+        halos = {r: self._buffer(self.halo, r, vp.ranks[r].halo_rows, ld) for r in self.local}
+        dst = [0] * self.grid.p
+        for r in self.local:
+            dst[r] = halos[r].data_ptr()
+        self._xchg(hs, dst, f, ld, st)
+        L.check(lib.dg_spmm_run_fused(
+            self._splan, L.ptr_array([hs[r] for r in self.local]),
+            L.ptr_array([halos[r] for r in self.local]), L.ptr_array([z[r] for r in self.local]),
+            L.ptr_array([h[r] for r in self.local]) if h is not None else None, f, ld, ld_out,
+            C.c_void_p(w.data_ptr()), w.stride(0), n_out, st))
+        return z
+
     # ---- pieces of a phase, for per-kernel timing in bench.py ------------
     def exchange_only(self, hs: dict, f: int, ld: int):
         """The halo exchange of one phase (+ the device barrier that makes

@@ -334,7 +334,7 @@ class GcnRun:
     reference where it precedes the epoch loop)."""
 
     def __init__(self, a_hat: CsrMatrix, features, labels, train_mask, cfg: TrainConfig, p=1,
-                 c=1, partition=None, row_order=None):
+                 c=1, partition=None, row_order=None, fuse=True):
         validate_variant_grid(cfg.variant, p, c)
         from .dist import world
         world().init()
@@ -376,6 +376,7 @@ class GcnRun:
         self.mask = torch.from_numpy(msk2.astype(np.uint8)).to(dev)
         self.xent = {}
         self.dense = {}
+        self.fuse = bool(fuse)        # fused SpMM + transform + ReLU where it applies
         self.ctx = {}                 # device state reused across runs (reduction slots)
         self.timer = None             # PhaseTimer for a breakdown run (bench)
         # register the device plans up front (multi-process: fixed IPC
@@ -386,6 +387,22 @@ class GcnRun:
         for op in {id(self.dm.fwd): self.dm.fwd, id(self.dm.bwd): self.dm.bwd}.values():
             op.row_order = row_order
             device_plan(op, grid, cfg.variant, max_ld=max(self.lds))
+
+    def _fusable(self, l):
+        """Layer l's forward transform (+ReLU) runs in the SpMM epilogue
+        (DevicePlan.run_fused): aggregate-first order, 1D or c=1, one
+        process (single-pass plans), 13..16-float inputs, <= 64 outputs.
+        Same numbers as SpMM -> dense_rows: T is summed identically and
+        z = t W accumulates in ascending k in fp32 in both."""
+        from .dist import world
+        cfg = self.cfg
+        if not self.fuse or world().multi or cfg.order != "aggregate-first":
+            return False
+        if cfg.reduce_after_transform and self.grid.c > 1:
+            return False
+        if not cfg.variant.startswith("1d") and self.grid.c > 1:
+            return False
+        return 13 <= self.dims[l] <= 16 and self.dims[l + 1] <= 64
 
     def _inputs(self, i):
         """Block row i of the features, labels and mask (device views)."""
@@ -442,6 +459,15 @@ class GcnRun:
                             h = torch.empty_like(z)
                             L.check(lib.dg_relu(z.data_ptr(), h.data_ptr(), z.shape[0],
                                                 dims[l + 1], lds[l + 1], st))
+                    elif self._fusable(l):
+                        # fused forward epilogue: T = A H stays in registers
+                        z = (arena.get("l", n_i, lds[l + 1]) if l == last else
+                             torch.empty((n_i, lds[l + 1]), dtype=torch.float32,
+                                         device=self.device))
+                        h = torch.empty_like(z) if l < last else None
+                        spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant,
+                                   fuse=(w, dims[l + 1], z, h))
+                        mark(f"fwd_spmm_f{dims[l]}_fused")
                     else:
                         t = spmm_phase(comm, dm.fwd, hs[-1], dims[l], cfg.variant,
                                        out=arena.get("t", n_i, lds[l]))
@@ -541,6 +567,21 @@ class GcnRun:
                 hs = {r: [blk[r][0]] for r in ranks}
                 zs = {r: [] for r in ranks}
                 for l in range(last + 1):
+                    if self._fusable(l):                # fused forward epilogue
+                        zz = {r: (arena[r].get("l", n_i[r], lds[l + 1]) if l == last else
+                                  torch.empty((n_i[r], lds[l + 1]), dtype=torch.float32,
+                                              device=self.device)) for r in ranks}
+                        hh = ({r: torch.empty_like(zz[r]) for r in ranks} if l < last
+                              else None)
+                        fwd.run_fused({r: hs[r][-1] for r in ranks}, dims[l], lds[l],
+                                      ws[ranks[0]][l], dims[l + 1], lds[l + 1], zz, hh)
+                        fwd.vplan.charge(ledger, dims[l])
+                        mark(f"fwd_spmm_f{dims[l]}_fused")
+                        for r in ranks:
+                            zs[r].append(zz[r])
+                            hs[r].append(hh[r] if l < last else zz[r])
+                        mark(f"fwd_dense_{l}")
+                        continue
                     t = fwd.run({r: hs[r][-1] for r in ranks}, dims[l], lds[l],
                                 out={r: arena[r].get("t", n_i[r], lds[l]) for r in ranks})
                     fwd.vplan.charge(ledger, dims[l])

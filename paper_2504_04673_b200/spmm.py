@@ -68,7 +68,8 @@ def device_plan(op: DistOperand, grid: ProcessGrid, variant: str, max_ld=None):
 
 
 def spmm_phase(comm: Comm, op: DistOperand, h_pad: torch.Tensor, f: int, variant: str,
-               reduce: bool = True, reduce_f: int = None, out: torch.Tensor = None):
+               reduce: bool = True, reduce_f: int = None, out: torch.Tensor = None,
+               fuse=None):
     """Device form of `spmm_kernel`: h_pad is a contiguous fp32 CUDA tensor
     (n_i, pad4(f)) with zero padding; returns the padded (n_i, pad4(f))
     product.  A collective over the ranks of this process: the last rank to
@@ -76,7 +77,11 @@ def spmm_phase(comm: Comm, op: DistOperand, h_pad: torch.Tensor, f: int, variant
     reduce=False (1.5D, extension): return each replica's partial product;
     the caller reduces after its transform and `reduce_f` is the width the
     ledger charges for that reduction.  `out` (optional): this rank's
-    (n_i, pad4(f)) output buffer (the GCN loop's activation arena)."""
+    (n_i, pad4(f)) output buffer (the GCN loop's activation arena).
+    `fuse` (optional, see `DevicePlan.run_fused`): (w, n_out, z, h) -- the
+    layer's transform and ReLU fused into the SpMM epilogue; every rank
+    passes its (bitwise identical) replica of w and its own z / h buffers;
+    returns z.  The phase and its ledger charges are unchanged."""
     grid = comm.grid
     ledger = comm.ledger
     ld = pad4(f)
@@ -84,18 +89,26 @@ def spmm_phase(comm: Comm, op: DistOperand, h_pad: torch.Tensor, f: int, variant
     def complete(arr):
         dp = device_plan(op, grid, variant, max_ld=ld)
         hs, outs = {}, {}
-        for r, (h, o) in arr.items():
+        for r, (h, o, _) in arr.items():
             hs[r] = h if (isinstance(h, torch.Tensor) and h.dtype == torch.float32
                           and h.is_cuda and h.is_contiguous() and h.shape[1] == ld) \
                 else to_device(h[:, :f], ld)
             outs[r] = o
-        given = all(o is not None for o in outs.values())
-        res = dp.run(hs, f, ld, out=outs if given else None, reduce=reduce)
+        if fuse is not None:
+            fz = {r: fu for r, (_, _, fu) in arr.items()}
+            w, n_out = fz[min(fz)][0], fz[min(fz)][1]
+            z = {r: v[2] for r, v in fz.items()}
+            hh = {r: v[3] for r, v in fz.items()}
+            res = dp.run_fused(hs, f, ld, w, n_out, int(z[min(z)].shape[1]), z,
+                               hh if all(v is not None for v in hh.values()) else None)
+        else:
+            given = all(o is not None for o in outs.values())
+            res = dp.run(hs, f, ld, out=outs if given else None, reduce=reduce)
         dp.vplan.charge(ledger, f, None if reduce else reduce_f)
         return res
 
-    return comm._collective(("spmm", id(op), variant, reduce), tuple(range(comm.p)),
-                            (h_pad, out), complete)
+    return comm._collective(("spmm", id(op), variant, reduce, fuse is not None),
+                            tuple(range(comm.p)), (h_pad, out, fuse), complete)
 
 
 def row_group_reduce(comm: Comm, u: torch.Tensor, dm: DistMatrices, variant: str):
