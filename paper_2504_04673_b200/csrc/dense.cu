@@ -713,8 +713,11 @@ static bool tn_tma_geom(int32_t K, int32_t N, TnGeom* g, int* kblocks) {
   return true;
 }
 
+#ifndef DG_TN_CTAS
+#define DG_TN_CTAS (4 * 148)
+#endif
 static int64_t tn_tma_slices(int64_t n, int kblocks, int RC) {
-  const int64_t want = std::max<int64_t>(1, (4 * 148) / kblocks);
+  const int64_t want = std::max<int64_t>(1, DG_TN_CTAS / kblocks);
   return std::max<int64_t>(1, std::min<int64_t>(want, (n + RC - 1) / RC));
 }
 

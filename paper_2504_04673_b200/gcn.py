@@ -396,7 +396,7 @@ class GcnRun:
         z = t W accumulates in ascending k in fp32 in both."""
         from .dist import world
         cfg = self.cfg
-        if not self.fuse or world().multi or cfg.order != "aggregate-first":
+        if not getattr(self, "fuse", True) or world().multi or cfg.order != "aggregate-first":
             return False
         if cfg.reduce_after_transform and self.grid.c > 1:
             return False
