@@ -1,4 +1,5 @@
 set -x
+timeout 900 python -m pytest tests/test_gpu_sharded.py tests/test_gpu_fused.py -x -q > gpurun_out/r2_sharded_tests.log 2>&1; echo "sharded tests $?"; tail -2 gpurun_out/r2_sharded_tests.log
 for lib in default tn2; do
   if [ $lib = default ]; then export DG_LIB_PATH=paper_2504_04673_b200/libdgb200.so; else export DG_LIB_PATH=paper_2504_04673_b200/libdgb200_$lib.so; fi
   echo "== $lib"
