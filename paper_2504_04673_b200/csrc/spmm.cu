@@ -189,7 +189,10 @@ __global__ void __launch_bounds__(256, MB)
   // (profiles/r02/r2_v2_*)
   const int nl32 = (int)nl;
   const int ld32 = (int)ld;
-  const float* hh_off = hh - nl * ld;       // halo row c lives at hh_off + c * ld
+  // halo row c lives at hh_off + c * ld (integer arithmetic: hh may be null
+  // when the rank has no halo, and then no c >= n_local occurs)
+  const float* hh_off =
+      reinterpret_cast<const float*>(reinterpret_cast<uintptr_t>(hh) - (uintptr_t)(nl * ld * 4));
   const uint64_t pol = evict_first_policy();
 
   int chk[CPL];                             // chunk index (units of V floats)
