@@ -36,6 +36,12 @@ ACC_FP64 = 1          # fp32 4-entry windows folded into fp64 accumulators
 ACC_TWO_LEVEL = 2     # two-level fp32 (<= 64 ulp of sum|terms| per item; rows >= 32 floats)
 MAX_CHUNK = 1024      # nonzeros per work item before a row is split
 SPMM_WINDOW_NNZ = 0   # entries per length-bucketing window of a plan (0: DG_SPMM_WINDOW_NNZ)
+# multi-process phases narrower than this run exchange -> barrier -> one
+# SpMM pass instead of overlapping the exchange with an own-block pass and
+# adding a halo pass: narrow exchanges are short, and the split costs a
+# second pass over nearly every row (products-shaped N=4: every row has halo
+# entries) plus a read-modify-write of Z
+OVERLAP_MIN_F = 64
 
 
 def pad4(f: int) -> int:
@@ -208,11 +214,16 @@ class DevicePlan:
         self.row_order = row_order
         orders = [rank_row_order(x, row_order, self.device) for x in ro]
         self.overlap = self.multi
+        self._fplan = None
         if self.overlap:
             self._splan = _make_spmm_plan([_Part(x, False) for x in ro], max_chunk,
                                           orders=orders)
             self._bplan = _make_spmm_plan([_Part(x, True) for x in ro], max_chunk,
                                           L.DG_PLAN_SKIP_EMPTY_ROWS, orders=orders)
+            if not any(isinstance(x.col_ext, torch.Tensor) for x in ro):
+                # single-pass plan for the narrow phases (OVERLAP_MIN_F); not
+                # for HBM-resident operands (papers scale: no room for a copy)
+                self._fplan = _make_spmm_plan(ro, max_chunk, orders=orders)
             # high priority: the exchange's blocks are dispatched ahead of the
             # own-block SpMM's (otherwise the 10^5-block SpMM grid starves it)
             self._side = torch.cuda.Stream(device=self.device, priority=-1)
@@ -242,7 +253,7 @@ class DevicePlan:
         self.partial = {r: None for r in self.local}
         self.parity = 0
         if max_ld is not None:                 # split-row buffers: no growth in the hot call
-            for h in (self._splan, self._bplan):
+            for h in (self._splan, self._bplan, self._fplan):
                 if h:
                     L.check(lib.dg_spmm_plan_reserve(h, int(max_ld)))
         info = (C.c_int64 * 8)()
@@ -305,7 +316,7 @@ class DevicePlan:
 
     def _destroy_plans(self):
         lib = L.lib()
-        for name in ("_splan", "_bplan", "_xplan"):
+        for name in ("_splan", "_bplan", "_fplan", "_xplan"):
             h = getattr(self, name, None)
             if h:
                 (lib.dg_xchg_plan_destroy if name == "_xplan" else lib.dg_spmm_plan_destroy)(h)
@@ -384,22 +395,30 @@ class DevicePlan:
         self.parity ^= 1
         dst = [self._halo_ptr(d, par) for d in range(p)]
         halo_ptrs = [self._halo_ptr(r, par) for r in self.local]
-        main = torch.cuda.current_stream()
-        self._side.wait_stream(main)                    # H is ready
-        with torch.cuda.stream(self._side):
-            if self.parities == 1:
-                # every peer has finished reading its (single) halo buffer
-                # in the previous phase before anyone overwrites it
-                self.world.barrier()
-            self._xchg(hs, dst, f, ld, L.stream_ptr(self._side))
-            self.world.barrier()                        # every peer's rows have landed
         zp = ([self._partial_ptr(r, par) for r in self.local] if self.reduce
               else [out[r].data_ptr() for r in self.local])
-        self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, st)       # own block
-        main.wait_stream(self._side)
-        self._spmm(self._bplan, hs, halo_ptrs, zp, f, ld, 1, st)       # halo rows, z +=
-        for r in self.local:                            # inputs in use on the side stream
-            hs[r].record_stream(self._side)
+        if self._fplan is not None and f < OVERLAP_MIN_F:
+            # narrow phase: exchange -> barrier -> one pass over all entries
+            if self.parities == 1:
+                self.world.barrier()
+            self._xchg(hs, dst, f, ld, st)
+            self.world.barrier()                        # every peer's rows have landed
+            self._spmm(self._fplan, hs, halo_ptrs, zp, f, ld, 0, st)
+        else:
+            main = torch.cuda.current_stream()
+            self._side.wait_stream(main)                # H is ready
+            with torch.cuda.stream(self._side):
+                if self.parities == 1:
+                    # every peer has finished reading its (single) halo buffer
+                    # in the previous phase before anyone overwrites it
+                    self.world.barrier()
+                self._xchg(hs, dst, f, ld, L.stream_ptr(self._side))
+                self.world.barrier()                    # every peer's rows have landed
+            self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, st)   # own block
+            main.wait_stream(self._side)
+            self._spmm(self._bplan, hs, halo_ptrs, zp, f, ld, 1, st)   # halo rows, z +=
+            for r in self.local:                        # inputs in use on the side stream
+                hs[r].record_stream(self._side)
         if self.reduce and not reduce:
             from .dist import _as_tensor
             return {r: _as_tensor(self._partial_ptr(r, par), vp.ranks[r].n_rows * ld,
