@@ -220,10 +220,9 @@ class DevicePlan:
                                           orders=orders)
             self._bplan = _make_spmm_plan([_Part(x, True) for x in ro], max_chunk,
                                           L.DG_PLAN_SKIP_EMPTY_ROWS, orders=orders)
-            if not any(isinstance(x.col_ext, torch.Tensor) for x in ro):
-                # single-pass plan for the narrow phases (OVERLAP_MIN_F); not
-                # for HBM-resident operands (papers scale: no room for a copy)
-                self._fplan = _make_spmm_plan(ro, max_chunk, orders=orders)
+            # single-pass plan for the narrow phases (OVERLAP_MIN_F): a second
+            # copy of the entries (papers scale: +6.7 GB per GPU of 180)
+            self._fplan = _make_spmm_plan(ro, max_chunk, orders=orders)
             # high priority: the exchange's blocks are dispatched ahead of the
             # own-block SpMM's (otherwise the 10^5-block SpMM grid starves it)
             self._side = torch.cuda.Stream(device=self.device, priority=-1)
@@ -472,10 +471,11 @@ class DevicePlan:
                                         L.ptr_array([out[r]]), 0, n, 0, st))
 
     def can_fuse(self, f, n_out):
-        """Whether `run_fused` applies: a single-pass plan (one process, no
-        own/halo split), no 1.5D partials, 13..16-float rows, n_out <= 64."""
-        return (not self.multi) and (not self.reduce) and 13 <= int(f) <= 16 and \
-            int(n_out) <= 64
+        """Whether `run_fused` applies: a single-pass phase (one process, or
+        a narrow multi-process phase on the single-pass plan), no 1.5D
+        partials, 13..16-float rows, n_out <= 64."""
+        single = (not self.multi) or (self._fplan is not None and int(f) < OVERLAP_MIN_F)
+        return single and (not self.reduce) and 13 <= int(f) <= 16 and int(n_out) <= 64
 
     def run_fused(self, hs: dict, f: int, ld: int, w, n_out: int, ld_out: int, z: dict,
                   h: dict = None):
@@ -489,14 +489,30 @@ class DevicePlan:
         lib = L.lib()
         st = _stream()
         vp = self.vplan
-        halos = {r: self._buffer(self.halo, r, vp.ranks[r].halo_rows, ld) for r in self.local}
-        dst = [0] * self.grid.p
-        for r in self.local:
-            dst[r] = halos[r].data_ptr()
-        self._xchg(hs, dst, f, ld, st)
+        if self.multi:                                  # IPC halos, as in run()
+            if ld > self.max_ld:
+                raise ValueError(f"row pitch {ld} exceeds the registered maximum {self.max_ld}")
+            par = self.parity
+            self.parity ^= 1
+            dst = [self._halo_ptr(d, par) for d in range(self.grid.p)]
+            halo_ptrs = [self._halo_ptr(r, par) for r in self.local]
+            if self.parities == 1:
+                self.world.barrier()
+            self._xchg(hs, dst, f, ld, st)
+            self.world.barrier()                        # every peer's rows have landed
+            plan = self._fplan
+        else:
+            halos = {r: self._buffer(self.halo, r, vp.ranks[r].halo_rows, ld)
+                     for r in self.local}
+            dst = [0] * self.grid.p
+            for r in self.local:
+                dst[r] = halos[r].data_ptr()
+            halo_ptrs = [halos[r].data_ptr() for r in self.local]
+            self._xchg(hs, dst, f, ld, st)
+            plan = self._splan
         L.check(lib.dg_spmm_run_fused(
-            self._splan, L.ptr_array([hs[r] for r in self.local]),
-            L.ptr_array([halos[r] for r in self.local]), L.ptr_array([z[r] for r in self.local]),
+            plan, L.ptr_array([hs[r] for r in self.local]),
+            L.ptr_array(halo_ptrs), L.ptr_array([z[r] for r in self.local]),
             L.ptr_array([h[r] for r in self.local]) if h is not None else None, f, ld, ld_out,
             C.c_void_p(w.data_ptr()), w.stride(0), n_out, st))
         return z

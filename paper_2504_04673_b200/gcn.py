@@ -390,19 +390,22 @@ class GcnRun:
 
     def _fusable(self, l):
         """Layer l's forward transform (+ReLU) runs in the SpMM epilogue
-        (DevicePlan.run_fused): aggregate-first order, 1D or c=1, one
-        process (single-pass plans), 13..16-float inputs, <= 64 outputs.
+        (DevicePlan.run_fused): aggregate-first order, 1D or c=1, a
+        single-pass phase, 13..16-float inputs, <= 64 outputs.
         Same numbers as SpMM -> dense_rows: T is summed identically and
         z = t W accumulates in ascending k in fp32 in both."""
-        from .dist import world
+        from .spmm import device_plan
         cfg = self.cfg
-        if not getattr(self, "fuse", True) or world().multi or cfg.order != "aggregate-first":
+        if not getattr(self, "fuse", True) or cfg.order != "aggregate-first":
             return False
         if cfg.reduce_after_transform and self.grid.c > 1:
             return False
         if not cfg.variant.startswith("1d") and self.grid.c > 1:
             return False
-        return 13 <= self.dims[l] <= 16 and self.dims[l + 1] <= 64
+        if not (13 <= self.dims[l] <= 16 and self.dims[l + 1] <= 64):
+            return False
+        return device_plan(self.dm.fwd, self.grid, cfg.variant).can_fuse(self.dims[l],
+                                                                         self.dims[l + 1])
 
     def _inputs(self, i):
         """Block row i of the features, labels and mask (device views)."""
