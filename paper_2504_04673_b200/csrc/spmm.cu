@@ -504,27 +504,32 @@ __global__ void __launch_bounds__(128) spmm_fixup_kernel(const __grid_constant__
   }
 }
 
-// fused epilogue for the split rows: t = the ordered sum of the row's
-// partials (as spmm_fixup_kernel), then z = t W, relu(z)
-__global__ void __launch_bounds__(128) spmm_fixup_fused_kernel(
-    const __grid_constant__ FixArgs a, const float* __restrict__ w, int ld_w, int n_out) {
-  __shared__ float t[16];
-  const Fixup fx = a.fix[blockIdx.x];
-  if (threadIdx.x < 16) {
-    double s = 0.0;
-    if (threadIdx.x < a.nfloat)
-      for (int k = 0; k < fx.n; ++k) s += a.part[(int64_t)(fx.slot0 + k) * a.ld_part + threadIdx.x];
-    t[threadIdx.x] = (float)s;
-  }
-  __syncthreads();
+// fused epilogue for the split rows: one warp per split row (8 per CTA);
+// lanes 0..15 form t = the ordered sum of the row's partials (as
+// spmm_fixup_kernel), broadcast by shuffles, then z = t W, relu(z)
+__global__ void __launch_bounds__(256) spmm_fixup_fused_kernel(
+    const __grid_constant__ FixArgs a, int64_t n_fix, const float* __restrict__ w, int ld_w,
+    int n_out) {
+  const int64_t fi = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (fi >= n_fix) return;
+  const int lane = threadIdx.x & 31;
+  const Fixup fx = a.fix[fi];
+  double s = 0.0;
+  if (lane < a.nfloat)
+    for (int k = 0; k < fx.n; ++k) s += a.part[(int64_t)(fx.slot0 + k) * a.ld_part + lane];
+  const float tl = lane < 16 ? (float)s : 0.f;
+  float t[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) t[k] = __shfl_sync(0xffffffffu, tl, k);
   float* zp = a.z[fx.rank] + (int64_t)fx.row * a.ld_z;
-  float* hp = a.hr[fx.rank];
-  for (int j = threadIdx.x; j < a.ld_z; j += blockDim.x) {
+  float* hp = a.hr[fx.rank] ? a.hr[fx.rank] + (int64_t)fx.row * a.ld_z : nullptr;
+  for (int j = lane; j < a.ld_z; j += 32) {
     float v = 0.f;
     if (j < n_out)
-      for (int k = 0; k < 16; ++k) v = fmaf(t[k], w[(int64_t)k * ld_w + j], v);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v = fmaf(t[k], __ldg(w + (int64_t)k * ld_w + j), v);
     zp[j] = v;
-    if (hp) hp[(int64_t)fx.row * a.ld_z + j] = fmaxf(v, 0.f);
+    if (hp) hp[j] = fmaxf(v, 0.f);
   }
 }
 
@@ -1111,7 +1116,8 @@ int dg_spmm_run_fused(dg_spmm_plan* p, const float* const* h_local, const float*
     fa.ld_part = ld_h;
     fa.nfloat = f;
     fa.beta = 0;
-    spmm_fixup_fused_kernel<<<(unsigned)p->n_fix, 128, 0, S(stream)>>>(fa, w, (int)ld_w, n_out);
+    spmm_fixup_fused_kernel<<<(unsigned)((p->n_fix + 7) / 8), 256, 0, S(stream)>>>(
+        fa, p->n_fix, w, (int)ld_w, n_out);
     DG_LAUNCHED();
   }
   return DG_OK;
