@@ -32,6 +32,13 @@
 
 #include <cstdlib>
 
+#ifndef DG_SPMM_HUB_ROWS
+// rows per rank kept in L1 by the wide (256-bit, staged) gathers, all other
+// wide gathers bypass L1: f=602 17.41 -> 17.19 ms, products f=100 4.76 ->
+// 4.62 ms (profiles/r02/r2_hub_*); 0 disables the flags
+#define DG_SPMM_HUB_ROWS 512
+#endif
+
 namespace {
 
 struct Item {          // 24 B: one row, or one fixed chunk of a long row
@@ -121,6 +128,15 @@ struct Vec<4> {
     v[2] = t.z;
     v[3] = t.w;
   }
+  // hub rows (flagged by the plan) stay in L1 (evict_last); every other
+  // gathered row bypasses it (no_allocate) so the hubs are not evicted
+  __device__ __forceinline__ void load_hint(const float* p, bool hub) {
+    asm("{\n .reg .pred h;\n setp.ne.b32 h, %5, 0;\n"
+        " @h ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];\n"
+        " @!h ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];\n}"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+        : "l"(p), "r"((int)hub));
+  }
   __device__ __forceinline__ void zero() {
 #pragma unroll
     for (int k = 0; k < 4; ++k) v[k] = 0.f;
@@ -134,6 +150,14 @@ struct Vec<8> {
         : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
           "=f"(v[7])
         : "l"(p));
+  }
+  __device__ __forceinline__ void load_hint(const float* p, bool hub) {
+    asm("{\n .reg .pred h;\n setp.ne.b32 h, %9, 0;\n"
+        " @h ld.global.nc.L1::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+        " @!h ld.global.nc.L1::no_allocate.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n}"
+        : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]),
+          "=f"(v[7])
+        : "l"(p), "r"((int)hub));
   }
   __device__ __forceinline__ void zero() {
 #pragma unroll
@@ -246,12 +270,14 @@ __global__ void __launch_bounds__(256, MB)
       float v[E];
   #pragma unroll
       for (int j = 0; j < E; ++j) {
-        const int c = (j & 1) ? cur[j >> 1].z : cur[j >> 1].x;
+        const int c = ((j & 1) ? cur[j >> 1].z : cur[j >> 1].x) & 0x7fffffff;  // bit 31: hub
         v[j] = __int_as_float((j & 1) ? cur[j >> 1].w : cur[j >> 1].y);
         if (j < nv) {
           const float* hp = (c < nl32 ? hl : hh_off) + (int64_t)c * ld32;
   #pragma unroll
           for (int q = 0; q < CPL; ++q) {
+            // narrow rows keep plain (L1-allocating) loads: their L1 hit rate
+            // is 13-14% and no_allocate cost f=41 1.54 -> 2.07 ms
             if (on[q]) x[j][q].load(hp + (int64_t)chk[q] * V);
             else x[j][q].zero();
           }
@@ -328,11 +354,11 @@ __global__ void __launch_bounds__(256, MB)
           const int2 en = win[st * E + j];
           v[j] = __int_as_float(en.y);
           if (j < nv) {
-            const int c = en.x;
+            const int c = en.x & 0x7fffffff;        // bit 31: a hub row (plan)
             const float* hp = (c < nl32 ? hl : hh_off) + (int64_t)c * ld32;
 #pragma unroll
             for (int q = 0; q < CPL; ++q) {
-              if (on[q]) x[j][q].load(hp + (int64_t)chk[q] * V);
+              if (on[q]) x[j][q].load_hint(hp + (int64_t)chk[q] * V, en.x < 0);
               else x[j][q].zero();
             }
           } else {
@@ -855,6 +881,27 @@ int dg_spmm_plan_create_ordered(dg_spmm_plan** out, int n_ranks, const int64_t* 
       p->items = d_items;
     }
   } else {
+    // hub rows: the DG_SPMM_HUB_ROWS most gathered columns of each rank get
+    // bit 31 of their entries set; the kernel keeps their rows in L1
+    // (evict_last) and lets every other gather bypass it
+    std::vector<std::vector<char>> hub(n_ranks);
+    for (int r = 0; r < n_ranks && DG_SPMM_HUB_ROWS > 0; ++r) {
+      const int64_t ext = p->ext_rows[r];
+      if (ext <= 0 || nnz[r] == 0) continue;
+      std::vector<int32_t> cnt(ext, 0);
+      for (int64_t k = 0; k < nnz[r]; ++k) ++cnt[col_ext[r][k]];
+      const int64_t K = std::min<int64_t>(DG_SPMM_HUB_ROWS, ext);
+      std::vector<int32_t> idx(ext);
+      for (int64_t i = 0; i < ext; ++i) idx[i] = (int32_t)i;
+      std::nth_element(idx.begin(), idx.begin() + (K - 1), idx.end(),
+                       [&](int32_t x, int32_t y) { return cnt[x] > cnt[y]; });
+      const int32_t kth = cnt[idx[K - 1]];
+      hub[r].assign(ext, 0);
+      // a hub must be gathered well above the average (>= 4x), else no flag
+      const double avg = (double)nnz[r] / (double)ext;
+      for (int64_t i = 0; i < K; ++i)
+        if (cnt[idx[i]] >= 4.0 * avg && cnt[idx[i]] >= kth) hub[r][idx[i]] = 1;
+    }
     std::vector<std::vector<int32_t>> host(n_ranks);
     for (int r = 0; r < n_ranks; ++r) host[r].assign(2 * std::max<int64_t>(total[r], 2), 0);
     for (Item& it : items) {
@@ -862,7 +909,8 @@ int dg_spmm_plan_create_ordered(dg_spmm_plan** out, int n_ranks, const int64_t* 
       const int64_t dst = cursor[r];
       int32_t* h = host[r].data() + 2 * dst;
       for (int32_t k = 0; k < it.len; ++k) {
-        h[2 * k] = col_ext[r][it.lo + k];
+        const int32_t cc = col_ext[r][it.lo + k];
+        h[2 * k] = (!hub[r].empty() && hub[r][cc]) ? (int32_t)(cc | 0x80000000u) : cc;
         float v = val[r][it.lo + k];
         std::memcpy(&h[2 * k + 1], &v, 4);
       }

@@ -1,0 +1,8 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_numerics.py tests/test_gpu_parity.py tests/test_gpu_locality.py tests/test_gpu_fused.py tests/test_gpu_fullsize.py -x -q > gpurun_out/r2_hub_tests.log 2>&1; echo "tests $?"; tail -2 gpurun_out/r2_hub_tests.log
+for lib in head default; do
+  if [ $lib = default ]; then export DG_LIB_PATH=paper_2504_04673_b200/libdgb200.so; else export DG_LIB_PATH=paper_2504_04673_b200/libdgb200_$lib.so; fi
+  echo "== $lib"
+  timeout 600 python scripts/prof_spmm.py --workload reddit --f 602 16 41 --reps 5 2>&1 | grep " ms"
+  timeout 600 python scripts/prof_spmm.py --workload products --f 100 16 47 --reps 5 --order lpa-part 2>&1 | grep " ms"
+done
