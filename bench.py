@@ -389,6 +389,23 @@ def reference_measure(args, wl, warmup, steps):
     sp = REF_SAMPLES[args.workload]
     p = min(cores, 16)
     deg = sp["nnz_full"] / sp["n_full"]
+    if getattr(args, "ref_full", False):
+        # the full-size graph through the unchanged reference: minutes per
+        # epoch, so only on request (validates the sample-based estimate);
+        # epoch 0 carries the reference's own setup and is dropped
+        a = _ref_csr(D, make_graph(args.workload))
+        x, y, _ = make_inputs(wl, a.n_rows)
+        log(f"[bench] reference, full graph: n={a.n_rows} nnz={a.nnz:,}, p={p} threads")
+        ep, _ = ref_epoch_times(D, a, x, y, cfg_kw, p, 1 + max(1, steps))
+        timed = ep[1:]
+        ms = statistics.median(timed) * 1e3
+        return dict(value=ms, ms=ms, kind="measured (full workload)", cores=p, timed=timed,
+                    sample=(f"full {args.workload}-shaped graph: unchanged distgcn.train "
+                            f"(baseline/_ref), {a.nnz:,} nnz, p={p} simulated ranks = {p} "
+                            f"threads, {args.variant}; epoch 0 (with the reference's setup) "
+                            f"dropped"),
+                    extra={"ref_p": p, "nnz": int(a.nnz),
+                           "setup_plus_first_epoch_s": round(ep[0], 1)})
 
     def sample_graph(ns):
         g = graphgen.chung_lu_host(ns, int(ns * deg / 2), alpha=sp["alpha"],
@@ -968,6 +985,9 @@ def main():
     ap.add_argument("--workload", default="reddit", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default="1d-sparse")
     ap.add_argument("--ref-budget", type=float, default=15.0)
+    ap.add_argument("--ref-full", action="store_true",
+                    help="--impl reference: time the unchanged reference on the FULL graph "
+                         "(minutes per epoch; validates the sample-based estimate)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ranks-per-gpu", type=int, default=None,
                     help="virtual ranks per GPU (default 1; rmat14: p=4 ranks in total, "
