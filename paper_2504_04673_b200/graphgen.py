@@ -285,12 +285,14 @@ def reddit_shaped_device(seed=0, n=232_965, nnz=114_848_856):
     return chung_lu_device(n, nnz // 2, alpha=0.6, max_weight=21_657, seed=seed)
 
 
-def products_shaped_device(seed=0, n=2_449_029, nnz=2 * 61_859_140, communities=256):
+def products_shaped_device(seed=0, n=2_449_029, nnz=2 * 61_859_140, communities=256,
+                           p_in=0.8):
     """Config 3/4 graph on the GPU: 2.45M vertices, 123.7M stored
-    off-diagonal nonzeros, power-law degrees inside hidden communities.
+    off-diagonal nonzeros, power-law degrees inside hidden communities
+    (a fraction p_in of the edges inside them).
     Returns (adjacency, planted community of every vertex)."""
     return chung_lu_device(n, nnz // 2, alpha=0.55, max_weight=17_481, seed=seed,
-                           communities=communities, p_in=0.8, return_communities=True)
+                           communities=communities, p_in=p_in, return_communities=True)
 
 
 # ---------------------------------------------------------------------------
