@@ -143,13 +143,22 @@ constexpr int TR_BM = 128;          // rows per tile
 constexpr int TR_BK = 32;           // columns per stage (one 128-byte swizzle span)
 constexpr int TR_STAGES = 4;
 constexpr int TR_STAGE_BYTES = TR_BM * TR_BK * 4;
+// rows per consumer thread for N <= 16: 4 rows x 4 columns (4 consumer
+// warps) read 8 shared-memory vectors per 64 FMAs instead of 6 per 32 -- the
+// kernel was bound by shared-memory wavefronts (ncu: MIO throttle); K=602
+// 0.191 -> 0.145 ms, K=100 0.382 -> 0.289 ms
+#ifndef DG_TR_RPT16
+#define DG_TR_RPT16 4
+#endif
 
-template <int NP>
-__global__ void __launch_bounds__(288, 2) dense_rows_tma_kernel(
+template <int NP, int RPT>
+__global__ void __launch_bounds__(32 * (TR_BM * 4 / RPT / 32 + 1), 2) dense_rows_tma_kernel(
     const __grid_constant__ CUtensorMap amap, int64_t n, int K, const float* __restrict__ B,
     int64_t ldb, int N, int transB, float* __restrict__ C, int64_t ldc,
     float* __restrict__ Crelu, const float* __restrict__ Zmask, int64_t ldm) {
   constexpr int TN = NP / 4;                         // columns per thread
+  constexpr int RSPAN = TR_BM / RPT;                 // row stride between a thread's rows
+  constexpr int CW = RSPAN * 4 / 32;                 // consumer warps
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B alignment of the ring (128-byte swizzle atoms), computed in the
   // shared window and applied as an offset to the shared array -- an integer
@@ -172,14 +181,14 @@ __global__ void __launch_bounds__(288, 2) dense_rows_tma_kernel(
   if (tid == 0) {
     for (int s = 0; s < TR_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 8);
+      mbar_init(&empty[s], CW);
     }
     fence_mbar_init();
   }
   __syncthreads();
   const int64_t ntiles = (n + TR_BM - 1) / TR_BM;
   const int warp = tid >> 5, lane = tid & 31;
-  if (warp == 8) {                                   // producer
+  if (warp == CW) {                                  // producer
     if (lane == 0) {
       int64_t it = 0;
       for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x)
@@ -194,12 +203,12 @@ __global__ void __launch_bounds__(288, 2) dense_rows_tma_kernel(
     return;
   }
   const int cg = tid & 3;                            // columns cg*TN .. cg*TN+TN-1
-  const int rg = tid >> 2;                           // rows rg, rg + 64 of the tile
+  const int rg = tid >> 2;                           // rows rg + RSPAN r of the tile
   int64_t it = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    float acc[2][TN];
+    float acc[RPT][TN];
 #pragma unroll
-    for (int r = 0; r < 2; ++r)
+    for (int r = 0; r < RPT; ++r)
 #pragma unroll
       for (int c = 0; c < TN; ++c) acc[r][c] = 0.f;
     for (int kc = 0; kc < nk; ++kc, ++it) {
@@ -209,10 +218,10 @@ __global__ void __launch_bounds__(288, 2) dense_rows_tma_kernel(
       const float* bk = Bs + (size_t)kc * TR_BK * NP + cg * TN;
 #pragma unroll
       for (int q = 0; q < TR_BK / 4; ++q) {
-        float4 a[2];
+        float4 a[RPT];
 #pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int row = rg + 64 * r;
+        for (int r = 0; r < RPT; ++r) {
+          const int row = rg + RSPAN * r;
           a[r] = *reinterpret_cast<const float4*>(st + row * 128 + ((q ^ (row & 7)) << 4));
         }
 #pragma unroll
@@ -226,12 +235,11 @@ __global__ void __launch_bounds__(288, 2) dense_rows_tma_kernel(
             b[4 * c4 + 2] = v.z;
             b[4 * c4 + 3] = v.w;
           }
-          const float a0 = kk == 0 ? a[0].x : kk == 1 ? a[0].y : kk == 2 ? a[0].z : a[0].w;
-          const float a1 = kk == 0 ? a[1].x : kk == 1 ? a[1].y : kk == 2 ? a[1].z : a[1].w;
 #pragma unroll
-          for (int c = 0; c < TN; ++c) {
-            acc[0][c] = fmaf(a0, b[c], acc[0][c]);
-            acc[1][c] = fmaf(a1, b[c], acc[1][c]);
+          for (int r = 0; r < RPT; ++r) {
+            const float ar = kk == 0 ? a[r].x : kk == 1 ? a[r].y : kk == 2 ? a[r].z : a[r].w;
+#pragma unroll
+            for (int c = 0; c < TN; ++c) acc[r][c] = fmaf(ar, b[c], acc[r][c]);
           }
         }
       }
@@ -239,8 +247,8 @@ __global__ void __launch_bounds__(288, 2) dense_rows_tma_kernel(
       if (lane == 0) mbar_arrive(&empty[slot]);
     }
 #pragma unroll
-    for (int r = 0; r < 2; ++r) {
-      const int64_t gr = t * TR_BM + rg + 64 * r;
+    for (int r = 0; r < RPT; ++r) {
+      const int64_t gr = t * TR_BM + rg + RSPAN * r;
       if (gr >= n) continue;
 #pragma unroll
       for (int c4 = 0; c4 < TN / 4; ++c4) {
@@ -644,14 +652,15 @@ int dg_dense_rows(const float* A, int64_t lda, int64_t n, int32_t K, const float
       const unsigned grid = (unsigned)std::min<int64_t>(ntiles, 2 * 148);
 #define DG_TR(np)                                                                           \
   do {                                                                                      \
+    constexpr int rpt = (np) <= 16 ? DG_TR_RPT16 : 2;                                       \
     static bool attr = false;                                                               \
     if (!attr) {                                                                            \
-      DG_CK(cudaFuncSetAttribute(dense_rows_tma_kernel<np>,                                 \
+      DG_CK(cudaFuncSetAttribute(dense_rows_tma_kernel<np, rpt>,                            \
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024)); \
       attr = true;                                                                          \
     }                                                                                       \
-    dense_rows_tma_kernel<np><<<grid, 288, smem, st>>>(amap, n, K, B, ldb, N, transB, C, ldc, \
-                                                        C_relu, z_mask, ld_mask);           \
+    dense_rows_tma_kernel<np, rpt><<<grid, 32 * (TR_BM * 4 / rpt / 32 + 1), smem, st>>>(    \
+        amap, n, K, B, ldb, N, transB, C, ldc, C_relu, z_mask, ld_mask);                    \
   } while (0)
       switch (NP) {
         case 16: DG_TR(16); break;
