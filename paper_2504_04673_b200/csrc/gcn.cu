@@ -189,30 +189,33 @@ __global__ void __launch_bounds__(256, (K <= 2 ? 3 : 2)) xent_vec_kernel(
         for (int e = 0; e < 4; ++e) m = fmaxf(m, v[u][k][e]);
       m = grp_max<G>(m);
       const int64_t lbl = labels[row];
+      const bool lin = lbl >= 0 && lbl < C;
+      // the label's logit straight from memory (an L1 hit: the row was just
+      // loaded) instead of a compare-and-select per element
+      const float xv = lin ? x[row * ld + lbl] : 0.f;
       // the exponentials (each in (0, 1]) summed in fp32: a lane's <= 4K
-      // terms, then a fixed xor tree over the G lanes (<= (4K + log2 G) ulp);
-      // the label's logit comes from its owner lane with one shuffle
-      float sl = 0.f, xv = 0.f;
-      int am = C;
+      // terms, then a fixed xor tree over the G lanes (<= (4K + log2 G) ulp).
+      // Columns past C hold -inf (see the loads), so they add exp(-inf) = 0
+      // and never equal the maximum of a row with a finite entry: no
+      // per-element class test.  argmax: the lane's first maximal element,
+      // tracked as an offset (4kG + e) so the select takes an immediate
+      float sl = 0.f;
+      int a = 4 * K * G;
+#pragma unroll
+      for (int k = K - 1; k >= 0; --k)
+#pragma unroll
+        for (int e = 3; e >= 0; --e)
+          if (v[u][k][e] == m) a = 4 * k * G + e;
 #pragma unroll
       for (int k = 0; k < K; ++k)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const int j = 4 * (lig + k * G) + e;
-          if (j < C) {
-            if (v[u][k][e] == m && j < am) am = j;
-            if (j == lbl) xv = v[u][k][e];
-            v[u][k][e] = expf(v[u][k][e] - m);
-            sl += v[u][k][e];
-          } else {
-            v[u][k][e] = 0.f;
-          }
+          v[u][k][e] = expf(v[u][k][e] - m);
+          sl += v[u][k][e];
         }
       const double s = (double)grp_sumf<G>(sl);
-      const int owner = (int)((lbl >> 2) % G);
-      const double xl =
-          (double)__shfl_sync(0xffffffffu, xv, ((threadIdx.x & 31) & ~(G - 1)) + owner) -
-          (double)m;
+      const double xl = (double)xv - (double)m;
+      int am = (a == 4 * K * G) ? C : min(4 * lig + a, C);
       am = grp_min<G>(am);
       const bool on = valid[u] && mask[row] != 0;
       // (softmax - onehot) / denom with one division per row: p_j/denom =
@@ -225,7 +228,6 @@ __global__ void __launch_bounds__(256, (K <= 2 ? 3 : 2)) xent_vec_kernel(
       const double scale =
           __shfl_sync(0xffffffffu, scale_l, (threadIdx.x & 31) & ~(G - 1));
       const float scale_f = (float)scale;
-      const double inv_d = 1.0 / denom;
       float4* gr = reinterpret_cast<float4*>(grad + row * ldg);
 #pragma unroll
       for (int k = 0; k < K; ++k) {
@@ -233,19 +235,19 @@ __global__ void __launch_bounds__(256, (K <= 2 ? 3 : 2)) xent_vec_kernel(
         if (valid[u] && c < gchunk) {
           float o[4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int j = 4 * c + e;
-            // fp32 product (<= 1.5 ulp); the label entry, where p - 1 may
-            // cancel, in fp64
-            float sm = v[u][k][e] * scale_f;
-            if (j == lbl) sm = (float)((double)v[u][k][e] * scale - inv_d);
-            o[e] = (on && j < C) ? sm : 0.f;
-          }
+          for (int e = 0; e < 4; ++e)   // fp32 product (<= 1.5 ulp)
+            o[e] = (on && 4 * c + e < C) ? v[u][k][e] * scale_f : 0.f;
           gr[c] = make_float4(o[0], o[1], o[2], o[3]);
         }
       }
       if (valid[u])
         for (int c = lig + K * G; c < gchunk; c += G) gr[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+      // the label entry, where p - 1 may cancel, in fp64; rewritten by the
+      // lane that stored its float4 (same-thread order: the later store wins)
+      if (on && lin && (int)(lbl >> 2) % G == lig) {
+        const float el = expf(xv - m);
+        grad[row * ldg + lbl] = (float)((double)el * scale - 1.0 / denom);
+      }
       if (on && lig == 0) {
         loss += log(s) - xl;
         corr += (am == lbl) ? 1.0 : 0.0;

@@ -92,3 +92,32 @@ def test_xent_against_torch(n, C):
     assert not g[:, C:].any()
     corr = int(((xd.argmax(1) == lab) & mask).sum())
     assert float(stats[1]) == corr
+
+
+@pytest.mark.parametrize("C", [3, 41, 47, 172])
+def test_xent_ties_and_pad_garbage(C):
+    """Tied maxima pick the first class (numpy argmax), -inf logits add
+    nothing, and NaN in the padding columns never reaches the outputs."""
+    torch.manual_seed(7 + C)
+    n, ld = 999, pad4(C) + 4
+    x = torch.full((n, ld), float("nan"), device="cuda")
+    x[:, :C] = torch.randint(0, 3, (n, C), device="cuda").float()
+    x[::5, C // 2] = float("-inf")
+    lab = torch.randint(0, C, (n,), device="cuda")
+    lab[::5] = (C // 2 + 1) % C                    # finite loss: the label logit is finite
+    mask = torch.rand(n, device="cuda") < 0.6
+    denom = int(mask.sum())
+    g = torch.full_like(x, float("nan"))
+    stats = torch.zeros(2, dtype=torch.float64, device="cuda")
+    _Xent(n, torch.device("cuda"))(x, C, lab, mask.to(torch.uint8), denom, g, stats)
+    xd = x[:, :C].double()
+    loss = -(torch.log_softmax(xd, 1)[mask, lab[mask]]).sum()
+    assert abs(float(stats[0]) - float(loss)) <= 1e-6 * abs(float(loss)) + 1e-9
+    gr = torch.softmax(xd, 1)
+    gr[torch.arange(n), lab] -= 1
+    gr = gr / denom * mask[:, None]
+    assert torch.allclose(g[:, :C].double(), gr, rtol=1e-5, atol=1e-7)
+    assert not g[:, C:].any()
+    first = xd.cpu().numpy().argmax(1)
+    corr = int(((torch.from_numpy(first).cuda() == lab) & mask).sum())
+    assert float(stats[1]) == corr
