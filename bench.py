@@ -730,7 +730,7 @@ def run_ours(args, wl):
     import paper_2504_04673_b200 as P
     from paper_2504_04673_b200 import _lib
     from paper_2504_04673_b200.dist import world
-    from paper_2504_04673_b200.engine import pad4
+    from paper_2504_04673_b200.engine import OVERLAP_MIN_F, pad4
     from paper_2504_04673_b200.gcn import GcnRun
     from paper_2504_04673_b200.plan import build_variant_plan
     from paper_2504_04673_b200.spmm import device_plan
@@ -831,6 +831,27 @@ def run_ours(args, wl):
     dp.spmm_only(hs, f0, ld0, zs)
     t_spmm = _timed(lambda: dp.spmm_only(hs, f0, ld0, zs), 3, w) / 1e3
     t_xchg = _timed(lambda: dp.exchange_only(hs, f0, ld0), 3, w) / 1e3 if p > 1 else None
+    narrow = None
+    if p > 1 and dims[1] < OVERLAP_MIN_F:
+        # one narrow (single-pass) phase taken apart: the exchange + barrier,
+        # each rank's SpMM alone (spread = load imbalance), the whole phase
+        f1, ld1 = dims[1], pad4(dims[1])
+        h1 = {r: torch.randn(hs[r].shape[0], ld1, device=hs[r].device) for r in dp.local}
+        z1 = {r: torch.empty_like(h1[r]) for r in dp.local}
+        dp.run(h1, f1, ld1, z1)
+        t_x1 = _timed(lambda: dp.exchange_only(h1, f1, ld1), 5, w)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            dp.spmm_only(h1, f1, ld1, z1)
+        e1.record()
+        torch.cuda.synchronize()
+        per_rank = w.all_gather_object(round(e0.elapsed_time(e1) / 5, 3))
+        t_ph = _timed(lambda: dp.run(h1, f1, ld1, z1), 5, w)
+        narrow = {"f": f1, "exchange_ms": round(t_x1, 3), "spmm_ms_per_process": per_rank,
+                  "phase_ms": round(t_ph, 3)}
+        del h1, z1
     tot_b, gather_b = 0, 0
     for r in dp.local:
         b, u, nnz, m = spmm_bytes(dp.vplan, r, f0)
@@ -961,6 +982,7 @@ def run_ours(args, wl):
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
         "cuda_graph": bool(use_graph),
+        "narrow_phase": narrow,
         "host_driver": ("graph" if use_graph else "") + ("+lockstep" if lockstep else "")
                        if (use_graph or lockstep) else "rank threads",
         "epoch_breakdown_ms": breakdown,

@@ -543,6 +543,9 @@ class DevicePlan:
             halo_ptrs = [self._buffer(self.halo, r, self.vplan.ranks[r].halo_rows,
                                       ld).data_ptr() for r in self.local]
         zp = [out[r].data_ptr() for r in self.local]
+        if self.multi and self._fplan is not None and f < OVERLAP_MIN_F:
+            self._spmm(self._fplan, hs, halo_ptrs, zp, f, ld, 0, _stream())   # as run()
+            return
         self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, _stream())
         if self._bplan is not None:
             self._spmm(self._bplan, hs, halo_ptrs, zp, f, ld, 1, _stream())
