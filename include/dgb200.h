@@ -141,7 +141,9 @@ int dg_group_reduce(int g, const float* const* src, int n_dst, float* const* dst
  *      one process per GPU).  flags[q] points at process q's flag array;
  *      each process writes `epoch` to slot `me` of every peer and waits for
  *      all slots of its own array to reach `epoch`.  Bounded by timeout_ns;
- *      on timeout sets *err_dev = 1 instead of hanging the GPU.          */
+ *      on timeout sets *err_dev = 1 and traps: the context faults, so no
+ *      later kernel computes on stale halos and the host's next
+ *      synchronisation reports the error (fail closed, no hang).         */
 int dg_barrier(uint64_t* const* flags, int n_procs, int me, uint64_t epoch,
                int64_t timeout_ns, int32_t* err_dev, void* stream);
 
@@ -149,7 +151,9 @@ int dg_barrier(uint64_t* const* flags, int n_procs, int me, uint64_t epoch,
  *      softmax cross-entropy; grad = (softmax - onehot) / denom on masked
  *      rows, 0 elsewhere; stats_out[0] += loss sum, stats_out[1] += correct
  *      (first-index argmax, like np.argmax).  Deterministic (fixed-order
- *      block reduction).  scratch: >= 2 * ceil(n / 8) + 2 doubles.        */
+ *      block reduction).  Labels of masked rows must lie in [0, C) (the
+ *      host validates them, as _xent_parts raises ValueError); unmasked
+ *      rows may carry any label.  scratch: >= 2 * ceil(n / 8) + 2 doubles. */
 int dg_xent(const float* logits, int64_t n, int32_t C, int64_t ld, const int64_t* labels,
             const uint8_t* mask, double denom, float* grad, int64_t ld_grad,
             double* scratch, uint32_t* counter, double* stats_out, void* stream);
