@@ -947,6 +947,9 @@ def run_ours(args, wl):
     gr.x = xbuf[0]
     h2d = sum(w.all_gather_object(sum(v.numel() * 4 for v in xh.values())))
 
+    # CTA cap of each process's overlapped exchange (engine.OVERLAP_XCHG_K)
+    xctas = w.all_gather_object(getattr(dp, "xchg_ctas", 0)) if w.multi else None
+
     # ---- CPU baseline (rank 0, N=1 only) --------------------------------
     cpu = None
     if lead and args.gpus == 1 and not args.no_cpu_baseline:
@@ -982,6 +985,7 @@ def run_ours(args, wl):
         "cpu_baseline": cpu,
         "gpu_launches": int(launches),
         "cuda_graph": bool(use_graph),
+        "overlap_xchg_ctas": xctas,
         "narrow_phase": narrow,
         "host_driver": ("graph" if use_graph else "") + ("+lockstep" if lockstep else "")
                        if (use_graph or lockstep) else "rank threads",

@@ -128,6 +128,13 @@ int dg_xchg_plan_destroy(dg_xchg_plan* plan);
 int dg_xchg_run(dg_xchg_plan* plan, const float* const* h_src, int n_src,
                 float* const* dst_bufs, int n_dst, int32_t f, int64_t ld, int32_t fence_sys,
                 void* stream);
+/* Same, with at most max_ctas CTAs in flight over all segments (0: the
+ * default, DG_XCHG_DEFAULT_CTAS).  An exchange overlapped with the
+ * own-block SpMM passes a small cap so the SpMM keeps most SMs.          */
+#define DG_XCHG_DEFAULT_CTAS 296   /* 2 per SM */
+int dg_xchg_run_ctas(dg_xchg_plan* plan, const float* const* h_src, int n_src,
+                     float* const* dst_bufs, int n_dst, int32_t f, int64_t ld,
+                     int32_t fence_sys, int32_t max_ctas, void* stream);
 
 /* ---- group all-reduce: replaces Comm.all_reduce_sum (runtime.py:437-466).
  * For elements [lo, hi): s = src[0] + src[1] + ... + src[g-1] (ascending

@@ -19,6 +19,7 @@ DG_MAX_LOCAL = 64
 DG_MAX_GROUP = 64
 DG_PLAN_SKIP_EMPTY_ROWS = 1
 DG_PLAN_DEVICE_SRC = 2
+DG_XCHG_DEFAULT_CTAS = 296     # include/dgb200.h
 
 _lock = threading.Lock()
 _lib = None
@@ -58,6 +59,8 @@ _SIGS = {
     "dg_xchg_plan_destroy": (C.c_int, [c_vp]),
     "dg_xchg_run": (C.c_int, [c_vp, c_vpp, C.c_int, c_vpp, C.c_int, C.c_int32, C.c_int64,
                               C.c_int32, c_vp]),
+    "dg_xchg_run_ctas": (C.c_int, [c_vp, c_vpp, C.c_int, c_vpp, C.c_int, C.c_int32, C.c_int64,
+                                   C.c_int32, C.c_int32, c_vp]),
     "dg_group_reduce": (C.c_int, [C.c_int, c_vpp, C.c_int, c_vpp, C.c_int64, C.c_int64,
                                   C.c_int32, c_vp]),
     "dg_barrier": (C.c_int, [c_vpp, C.c_int, C.c_int, C.c_uint64, C.c_int64, c_vp, c_vp]),

@@ -135,6 +135,12 @@ int dg_xchg_plan_destroy(dg_xchg_plan* p) {
 
 int dg_xchg_run(dg_xchg_plan* p, const float* const* h_src, int n_src, float* const* dst_bufs,
                 int n_dst, int32_t f, int64_t ld, int32_t fence_sys, void* stream) {
+  return dg_xchg_run_ctas(p, h_src, n_src, dst_bufs, n_dst, f, ld, fence_sys, 0, stream);
+}
+
+int dg_xchg_run_ctas(dg_xchg_plan* p, const float* const* h_src, int n_src,
+                     float* const* dst_bufs, int n_dst, int32_t f, int64_t ld,
+                     int32_t fence_sys, int32_t max_ctas, void* stream) {
   if (!p) return set_err(DG_ERR_ARG, "xchg_run: null plan");
   if (p->n_segs == 0 || p->max_count == 0) return DG_OK;
   if (n_src < p->max_src || n_dst < p->max_dst || n_src > DG_MAX_LOCAL ||
@@ -155,7 +161,13 @@ int dg_xchg_run(dg_xchg_plan* p, const float* const* h_src, int n_src, float* co
   const int cpl = (a.chunks + G - 1) / G;
   const int64_t per_block = 256 / G;
   int64_t gx = (p->max_count + per_block - 1) / per_block;
-  gx = std::min<int64_t>(std::max<int64_t>(gx, 1), 16 * 148);
+  // CTAs in flight across all segments: a flooding grid (thousands of
+  // CTAs of a few rows each) was slower even alone (products rows at f=16:
+  // 0.099 ms uncapped vs 0.063 ms at 192 CTAs), and beside the own-block
+  // SpMM of an overlapped phase it takes every SM first -- the caller caps
+  // it lower there (profiles/r02/xchg_cap/)
+  const int cap = max_ctas > 0 ? max_ctas : DG_XCHG_DEFAULT_CTAS;
+  gx = std::min<int64_t>(std::max<int64_t>(gx, 1), std::max(1, cap / std::max(1, p->n_segs)));
   dim3 grid((unsigned)gx, (unsigned)p->n_segs);
   cudaStream_t st = S(stream);
 #define DG_X(g, c) xchg_kernel<g, c><<<grid, 256, 0, st>>>(a)

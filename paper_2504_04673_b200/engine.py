@@ -42,6 +42,17 @@ SPMM_WINDOW_NNZ = 0   # entries per length-bucketing window of a plan (0: DG_SPM
 # second pass over nearly every row (products-shaped N=4: every row has halo
 # entries) plus a read-modify-write of Z
 OVERLAP_MIN_F = 64
+# CTAs of an exchange overlapped with the own-block SpMM (all segments).
+# The default grid takes every SM before the SpMM starts, serialising the
+# two; a capped one moves ~4.8 GB/s per CTA (products rows, 4 GPUs: 230 GB/s
+# at 48 CTAs, 445 at 96, 545 at 192).  The cap is sized so the exchange
+# ends about when the own-block pass does: both scale with the row width,
+# so cap ~ K * rows exchanged / own-block entries (Reddit-shaped N=4:
+# ratio 0.024, best cap 48-96, epoch 6.53 -> 6.09 ms; products-shaped
+# N=4: ratio ~0.06, where 48 CTAs made the exchange 2.5x longer than the
+# pass it hides behind; profiles/r02/xchg_cap/)
+OVERLAP_XCHG_K = 2500
+OVERLAP_XCHG_MIN_CTAS = 32
 
 
 def pad4(f: int) -> int:
@@ -237,6 +248,17 @@ class DevicePlan:
         segs.sort(key=lambda sg: ((w.proc_of(sg.dst, p) - w.proc_of(sg.src, p)) % w.size,
                                   (sg.dst - sg.src) % p, sg.src))
         self._segs = segs
+        self.xchg_ctas = 0                      # the library default
+        if self.overlap:
+            me = w.proc
+            own = sum(int((x.col_ext < x.n_local).sum()) for x in ro)
+            out_rows = sum(s.count for s in segs if w.proc_of(s.dst, p) != me)
+            in_rows = sum(s.count for s in vplan.segments
+                          if s.dst in self.li and w.proc_of(s.src, p) != me)
+            if own > 0:
+                self.xchg_ctas = int(min(L.DG_XCHG_DEFAULT_CTAS, max(
+                    OVERLAP_XCHG_MIN_CTAS,
+                    round(OVERLAP_XCHG_K * max(in_rows, out_rows) / own))))
         xh = C.c_void_p()
         L.check(lib.dg_xchg_plan_create(
             C.byref(xh), len(segs), L.i32_array([self.li[s.src] for s in segs]),
@@ -340,11 +362,11 @@ class DevicePlan:
                                     L.ptr_array(halo_ptrs), L.ptr_array(zp), f, ld, ld, self.acc,
                                     0, beta, stream))
 
-    def _xchg(self, hs, dst, f, ld, stream):
+    def _xchg(self, hs, dst, f, ld, stream, ctas=0):
         if self._segs:
-            L.check(L.lib().dg_xchg_run(self._xplan, L.ptr_array([hs[r] for r in self.local]),
-                                        len(self.local), L.ptr_array(dst), len(dst), f, ld,
-                                        1 if self.multi else 0, stream))
+            L.check(L.lib().dg_xchg_run_ctas(self._xplan, L.ptr_array([hs[r] for r in self.local]),
+                                             len(self.local), L.ptr_array(dst), len(dst), f, ld,
+                                             1 if self.multi else 0, ctas, stream))
 
     def run(self, hs: dict, f: int, ld: int, out: dict = None, reduce: bool = True) -> dict:
         """One multiply phase.  hs[r]: (n_i, ld) fp32 CUDA tensor for every
@@ -411,7 +433,7 @@ class DevicePlan:
                     # every peer has finished reading its (single) halo buffer
                     # in the previous phase before anyone overwrites it
                     self.world.barrier()
-                self._xchg(hs, dst, f, ld, L.stream_ptr(self._side))
+                self._xchg(hs, dst, f, ld, L.stream_ptr(self._side), self.xchg_ctas)
                 self.world.barrier()                    # every peer's rows have landed
             self._spmm(self._splan, hs, halo_ptrs, zp, f, ld, 0, st)   # own block
             main.wait_stream(self._side)

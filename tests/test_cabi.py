@@ -23,3 +23,14 @@ def test_version_and_launch_counter():
     h = _lib.load_library()
     assert h.dg_version() >= 1
     assert h.dg_launch_count() >= 0
+
+
+def test_header_constants_mirrored():
+    """Every DG_* constant the Python side mirrors equals the header's."""
+    hdr = open(os.path.join(ROOT, "include", "dgb200.h")).read()
+    defs = {k: v for k, v in re.findall(r"^#define\s+(DG_\w+)\s+\(?([0-9xXa-fA-F]+)", hdr, re.M)}
+    mirrored = [k for k in dir(_lib) if k.startswith("DG_") and isinstance(getattr(_lib, k), int)
+                and k in defs]
+    assert "DG_XCHG_DEFAULT_CTAS" in mirrored
+    for k in mirrored:
+        assert getattr(_lib, k) == int(defs[k], 0), k
