@@ -128,10 +128,9 @@ int dg_xchg_plan_destroy(dg_xchg_plan* plan);
 int dg_xchg_run(dg_xchg_plan* plan, const float* const* h_src, int n_src,
                 float* const* dst_bufs, int n_dst, int32_t f, int64_t ld, int32_t fence_sys,
                 void* stream);
-/* Same, with at most max_ctas CTAs in flight over all segments (0: the
- * default, DG_XCHG_DEFAULT_CTAS).  An exchange overlapped with the
- * own-block SpMM passes a small cap so the SpMM keeps most SMs.          */
-#define DG_XCHG_DEFAULT_CTAS 296   /* 2 per SM */
+/* Same, with at most max_ctas CTAs in flight over all segments (0: no cap,
+ * as dg_xchg_run).  An exchange overlapped with the own-block SpMM passes a
+ * cap so the SpMM keeps most SMs.                                        */
 int dg_xchg_run_ctas(dg_xchg_plan* plan, const float* const* h_src, int n_src,
                      float* const* dst_bufs, int n_dst, int32_t f, int64_t ld,
                      int32_t fence_sys, int32_t max_ctas, void* stream);

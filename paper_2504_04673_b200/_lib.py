@@ -19,7 +19,6 @@ DG_MAX_LOCAL = 64
 DG_MAX_GROUP = 64
 DG_PLAN_SKIP_EMPTY_ROWS = 1
 DG_PLAN_DEVICE_SRC = 2
-DG_XCHG_DEFAULT_CTAS = 296     # include/dgb200.h
 
 _lock = threading.Lock()
 _lib = None

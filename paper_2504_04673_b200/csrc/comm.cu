@@ -161,13 +161,14 @@ int dg_xchg_run_ctas(dg_xchg_plan* p, const float* const* h_src, int n_src,
   const int cpl = (a.chunks + G - 1) / G;
   const int64_t per_block = 256 / G;
   int64_t gx = (p->max_count + per_block - 1) / per_block;
-  // CTAs in flight across all segments: a flooding grid (thousands of
-  // CTAs of a few rows each) was slower even alone (products rows at f=16:
-  // 0.099 ms uncapped vs 0.063 ms at 192 CTAs), and beside the own-block
-  // SpMM of an overlapped phase it takes every SM first -- the caller caps
-  // it lower there (profiles/r02/xchg_cap/)
-  const int cap = max_ctas > 0 ? max_ctas : DG_XCHG_DEFAULT_CTAS;
-  gx = std::min<int64_t>(std::max<int64_t>(gx, 1), std::max(1, cap / std::max(1, p->n_segs)));
+  gx = std::min<int64_t>(std::max<int64_t>(gx, 1), 16 * 148);
+  // max_ctas: CTAs in flight across all segments.  Uncapped (0), the grid
+  // keeps thousands of rows in flight -- what an exchange whose source rows
+  // come from DRAM needs (papers-shaped: a 296-CTA grid halved its NVLink
+  // rate) -- but beside the own-block SpMM of an overlapped phase it takes
+  // every SM first; the caller caps it there (profiles/r02/xchg_cap/)
+  if (max_ctas > 0)
+    gx = std::min<int64_t>(gx, std::max(1, max_ctas / std::max(1, p->n_segs)));
   dim3 grid((unsigned)gx, (unsigned)p->n_segs);
   cudaStream_t st = S(stream);
 #define DG_X(g, c) xchg_kernel<g, c><<<grid, 256, 0, st>>>(a)

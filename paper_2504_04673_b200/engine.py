@@ -53,6 +53,11 @@ OVERLAP_MIN_F = 64
 # pass it hides behind; profiles/r02/xchg_cap/)
 OVERLAP_XCHG_K = 2500
 OVERLAP_XCHG_MIN_CTAS = 32
+# above this the exchange dominates the phase: no cap (the full grid keeps
+# the most rows in flight -- papers-shaped sources stream from DRAM)
+OVERLAP_XCHG_MAX_CTAS = 296
+NARROW_XCHG_CTAS = 296                 # 2 per SM
+NARROW_XCHG_L2_BYTES = 64 << 20
 
 
 def pad4(f: int) -> int:
@@ -248,7 +253,7 @@ class DevicePlan:
         segs.sort(key=lambda sg: ((w.proc_of(sg.dst, p) - w.proc_of(sg.src, p)) % w.size,
                                   (sg.dst - sg.src) % p, sg.src))
         self._segs = segs
-        self.xchg_ctas = 0                      # the library default
+        self.xchg_ctas = 0                      # 0: no cap
         if self.overlap:
             me = w.proc
             own = sum(int((x.col_ext < x.n_local).sum()) for x in ro)
@@ -256,9 +261,9 @@ class DevicePlan:
             in_rows = sum(s.count for s in vplan.segments
                           if s.dst in self.li and w.proc_of(s.src, p) != me)
             if own > 0:
-                self.xchg_ctas = int(min(L.DG_XCHG_DEFAULT_CTAS, max(
-                    OVERLAP_XCHG_MIN_CTAS,
-                    round(OVERLAP_XCHG_K * max(in_rows, out_rows) / own))))
+                cap = max(OVERLAP_XCHG_MIN_CTAS,
+                          round(OVERLAP_XCHG_K * max(in_rows, out_rows) / own))
+                self.xchg_ctas = int(cap) if cap <= OVERLAP_XCHG_MAX_CTAS else 0
         xh = C.c_void_p()
         L.check(lib.dg_xchg_plan_create(
             C.byref(xh), len(segs), L.i32_array([self.li[s.src] for s in segs]),
@@ -362,6 +367,13 @@ class DevicePlan:
                                     L.ptr_array(halo_ptrs), L.ptr_array(zp), f, ld, ld, self.acc,
                                     0, beta, stream))
 
+    def _narrow_ctas(self, ld):
+        """CTA cap of a narrow (single-pass) exchange: with the hosted H rows
+        L2-resident, 2 CTAs per SM beat the flooding grid (products rows at
+        f=16: 0.099 -> 0.06 ms); rows streamed from DRAM keep it uncapped."""
+        rows = sum(self.vplan.ranks[r].n_rows for r in self.local)
+        return NARROW_XCHG_CTAS if rows * ld * 4 <= NARROW_XCHG_L2_BYTES else 0
+
     def _xchg(self, hs, dst, f, ld, stream, ctas=0):
         if self._segs:
             L.check(L.lib().dg_xchg_run_ctas(self._xplan, L.ptr_array([hs[r] for r in self.local]),
@@ -422,7 +434,7 @@ class DevicePlan:
             # narrow phase: exchange -> barrier -> one pass over all entries
             if self.parities == 1:
                 self.world.barrier()
-            self._xchg(hs, dst, f, ld, st)
+            self._xchg(hs, dst, f, ld, st, self._narrow_ctas(ld))
             self.world.barrier()                        # every peer's rows have landed
             self._spmm(self._fplan, hs, halo_ptrs, zp, f, ld, 0, st)
         else:
@@ -520,7 +532,7 @@ class DevicePlan:
             halo_ptrs = [self._halo_ptr(r, par) for r in self.local]
             if self.parities == 1:
                 self.world.barrier()
-            self._xchg(hs, dst, f, ld, st)
+            self._xchg(hs, dst, f, ld, st, self._narrow_ctas(ld))
             self.world.barrier()                        # every peer's rows have landed
             plan = self._fplan
         else:
