@@ -39,21 +39,35 @@ __global__ void __launch_bounds__(256) xchg_kernel(const __grid_constant__ XArgs
   const float4* __restrict__ src = reinterpret_cast<const float4*>(a.src[sg.src_local]);
   float4* dst = reinterpret_cast<float4*>(a.dst[sg.dst_buf]);
   const int64_t ld4 = a.ld / 4;
-  for (int64_t k = blockIdx.x * per_block + threadIdx.x / G; k < sg.count;
-       k += (int64_t)gridDim.x * per_block) {
+  // two rows per group per step: both rows' loads are issued before either
+  // row's stores, so a capped grid (few CTAs beside an overlapped SpMM)
+  // still keeps enough DRAM / L2 reads in flight
+  const int64_t stride = (int64_t)gridDim.x * per_block;
+  for (int64_t k = blockIdx.x * per_block + threadIdx.x / G; k < sg.count; k += 2 * stride) {
+    const int64_t k2 = k + stride;
+    const bool two = k2 < sg.count;
     const int64_t srow = sg.idx ? (int64_t)__ldg(sg.idx + k) : sg.src_row0 + k;
+    const int64_t srow2 = two ? (sg.idx ? (int64_t)__ldg(sg.idx + k2) : sg.src_row0 + k2) : srow;
     const float4* s = src + srow * ld4;
-    float4* d = dst + (sg.dst_row0 + k) * ld4;
-    float4 v[CPL];
+    const float4* s2 = src + srow2 * ld4;
+    float4 v[CPL], v2[CPL];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       const int c = lig + q * G;
-      if (c < a.chunks) v[q] = __ldg(s + c);
+      if (c < a.chunks) {
+        v[q] = __ldg(s + c);
+        if (two) v2[q] = __ldg(s2 + c);
+      }
     }
+    float4* d = dst + (sg.dst_row0 + k) * ld4;
+    float4* d2 = dst + (sg.dst_row0 + k2) * ld4;
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       const int c = lig + q * G;
-      if (c < a.chunks) d[c] = v[q];
+      if (c < a.chunks) {
+        d[c] = v[q];
+        if (two) d2[c] = v2[q];
+      }
     }
   }
   if (a.fence_sys) __threadfence_system();

@@ -44,14 +44,14 @@ SPMM_WINDOW_NNZ = 0   # entries per length-bucketing window of a plan (0: DG_SPM
 OVERLAP_MIN_F = 64
 # CTAs of an exchange overlapped with the own-block SpMM (all segments).
 # The default grid takes every SM before the SpMM starts, serialising the
-# two; a capped one moves ~4.8 GB/s per CTA (products rows, 4 GPUs: 230 GB/s
-# at 48 CTAs, 445 at 96, 545 at 192).  The cap is sized so the exchange
-# ends about when the own-block pass does: both scale with the row width,
-# so cap ~ K * rows exchanged / own-block entries (Reddit-shaped N=4:
-# ratio 0.024, best cap 48-96, epoch 6.53 -> 6.09 ms; products-shaped
-# N=4: ratio ~0.06, where 48 CTAs made the exchange 2.5x longer than the
-# pass it hides behind; profiles/r02/xchg_cap/)
-OVERLAP_XCHG_K = 2500
+# two; a capped one (two rows in flight per lane group) moves ~6 GB/s per
+# CTA (products rows, 4 GPUs: 319 GB/s at 48 CTAs, 596 at 96).  The cap is
+# sized so the exchange ends about when the own-block pass does: both
+# scale with the row width, so cap ~ K * rows exchanged / own-block entries
+# (Reddit-shaped N=4: ratio 0.024; products-shaped N=4: ~0.057).  K sweep
+# at N=4 (f=602 / f=100 phase ms): 1500 -> 4.73 / 1.97, 2500 -> 4.79 /
+# 2.18, 4000 -> 4.88 / 2.21 (profiles/r02/xchg_cap/)
+OVERLAP_XCHG_K = 1500
 OVERLAP_XCHG_MIN_CTAS = 32
 # above this the exchange dominates the phase: no cap (the full grid keeps
 # the most rows in flight -- papers-shaped sources stream from DRAM)

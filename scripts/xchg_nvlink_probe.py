@@ -27,6 +27,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--rows", type=int, default=306_128)      # one products block at p=8
+    ap.add_argument("--ctas", type=int, default=0,
+                    help="CTA cap over all segments (dg_xchg_run_ctas; 0: none)")
     args = ap.parse_args()
     ng = torch.cuda.device_count()
     if ng < 2:
@@ -56,8 +58,8 @@ def main():
         st = torch.cuda.current_stream(0)
 
         def go():
-            L.check(lib.dg_xchg_run(xh, L.ptr_array([h]), 1, L.ptr_array(halo), n, f, ld, 1,
-                                    C.c_void_p(st.cuda_stream)))
+            L.check(lib.dg_xchg_run_ctas(xh, L.ptr_array([h]), 1, L.ptr_array(halo), n, f, ld,
+                                         1, args.ctas, C.c_void_p(st.cuda_stream)))
         go()
         for d in range(ng):
             torch.cuda.synchronize(d)
