@@ -52,7 +52,7 @@ OVERLAP_MIN_F = 64
 # at N=4 (f=602 / f=100 phase ms): 1500 -> 4.73 / 1.97, 2500 -> 4.79 /
 # 2.18, 4000 -> 4.88 / 2.21 (profiles/r02/xchg_cap/)
 OVERLAP_XCHG_K = 1500
-OVERLAP_XCHG_MIN_CTAS = 32
+OVERLAP_XCHG_MIN_CTAS = 48
 # above this the exchange dominates the phase: no cap (the full grid keeps
 # the most rows in flight -- papers-shaped sources stream from DRAM)
 OVERLAP_XCHG_MAX_CTAS = 296
